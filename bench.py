@@ -1,0 +1,398 @@
+"""Benchmark: box sums on B200 (the driver's contract).
+
+Workload (N=1 headline): BASELINE config 4 -- float32 1024x1024x1024 (4 GiB),
+values uniform [0,1), box (16,16,16), strong excluded sum via
+box-complement (the route the config names first; BDBSC is reported beside
+it under "routes").  A step is one box_complement_excluded call over the whole
+array with the input already resident in HBM.  The input (4 GiB) is 32x the
+126 MB L2, so no L2 flush is needed between steps.
+
+Multi-GPU (torchrun, one process per GPU): the array is sharded along axis 0
+(strong scaling of the fixed 1024^3 array); every rank runs the sharded
+route (halo + carry exchange over NCCL, paper_2106_00124_b200/sharded.py) on
+its slab and the step time is the max over ranks.
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--route box-complement|bdbsc|bdbs]
+    python bench.py --impl reference ...   # the CPU reference arm (oracle port)
+
+Prints ONE JSON line on rank 0.
+"""
+
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+CONFIGS = {
+    # name: (extents, dtype, box, value distribution, description)
+    "c4": ((1024, 1024, 1024), "float32", (16, 16, 16), "uniform01",
+           "C4 3-D FMM-like excluded sum, float32 1024^3 uniform[0,1), box 16^3"),
+    "c2": ((256, 256, 256), "int64", (8, 8, 8), "int20",
+           "C2 3-D excluded sums, int64 256^3 uniform[-2^20,2^20), box 8^3"),
+    "c1": ((1024, 1024), "float64", (32, 32), "uniform01",
+           "C1 2-D included sum, float64 1024^2 uniform[0,1), box 32^2"),
+}
+METRIC = "box-sum elements/s"
+UNIT = "elements/s"
+
+
+def _peaks():
+    try:
+        with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as f:
+            p = json.load(f)
+        return float(p["hbm_gbs"]), "measured"
+    except Exception:
+        return 6650.0, "fallback"
+
+
+class ClockSampler:
+    """nvidia-smi clocks/throttle reasons sampled during the timed region."""
+
+    FIELDS = ("clocks.sm,clocks.max.sm,clocks_event_reasons.hw_slowdown,"
+              "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
+              "clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, index: int):
+        self.index = index
+        self.proc = None
+        self.lines = []
+
+    def __enter__(self):
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", "-i", str(self.index), f"--query-gpu={self.FIELDS}",
+                 "--format=csv,noheader,nounits", "-lms", "100"],
+                stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            self.thread = threading.Thread(target=self._read, daemon=True)
+            self.thread.start()
+        except Exception:
+            self.proc = None
+        return self
+
+    def _read(self):
+        for line in self.proc.stdout:
+            self.lines.append(line.strip())
+
+    def __exit__(self, *exc):
+        if self.proc is not None:
+            self.proc.terminate()
+            try:
+                self.proc.wait(timeout=5)
+            except Exception:
+                self.proc.kill()
+
+    def summary(self):
+        sms, mx, reasons = [], None, set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for ln in self.lines:
+            parts = [p.strip() for p in ln.split(",")]
+            if len(parts) < 6:
+                continue
+            try:
+                sms.append(float(parts[0]))
+                mx = float(parts[1])
+            except ValueError:
+                continue
+            for nm, v in zip(names, parts[2:6]):
+                if v.lower().startswith("active"):
+                    reasons.add(nm)
+        if not sms:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": [], "samples": 0}
+        return {"sm_mhz": statistics.median(sms), "sm_max_mhz": mx, "reasons": sorted(reasons),
+                "samples": len(sms)}
+
+
+def make_input(cfg, device, seed=0, shape=None):
+    import torch
+
+    ext, dtype, box, dist, _ = CONFIGS[cfg]
+    shape = shape or ext
+    g = torch.Generator(device=device).manual_seed(seed)
+    if dist == "uniform01":
+        tdt = torch.float32 if dtype == "float32" else torch.float64
+        return torch.rand(shape, generator=g, device=device, dtype=tdt)
+    return torch.randint(-2**20, 2**20, shape, generator=g, device=device, dtype=torch.int64)
+
+
+def ops_for(ex, dtype, route):
+    if dtype == "float32":
+        return ex.Float32AddOps()
+    if dtype == "float64":
+        return ex.FloatAddOps()
+    return ex.IntMaxOps() if route == "box-complement" else ex.IntAddOps()
+
+
+def cpu_sample(cfg, route, nthreads, planes=64, reps=1):
+    """Time the CPU oracle port (oracle/, the reference algorithm restated in C
+    with OpenMP over independent lines) on a bounded sample of the workload:
+    the first `planes` planes along axis 0 (same trailing shape, same value
+    distribution, same box).  Returns elements/s."""
+    from oracle import oracle as orc
+
+    ext, dtype, box, dist, _ = CONFIGS[cfg]
+    shape = (min(planes, ext[0]),) + tuple(ext[1:])
+    rng = np.random.default_rng(0)
+    if dist == "uniform01":
+        a = rng.random(shape, dtype=np.float32 if dtype == "float32" else np.float64)
+    else:
+        a = rng.integers(-2**20, 2**20, size=shape, dtype=np.int64)
+    op = "max" if (dtype == "int64" and route == "box-complement") else "add"
+    fn = orc.ROUTES[route]
+    best = []
+    for _ in range(reps):
+        t0 = time.perf_counter()
+        fn(a, box, op, nthreads)
+        best.append(time.perf_counter() - t0)
+    dt = statistics.median(best)
+    return a.size / dt, shape, dt
+
+
+def run_reference(args, rank, world):
+    """--impl reference: the reference's CPU algorithm (oracle port) on host cores."""
+    if rank != 0:
+        return
+    cfg = args.config
+    nthreads = os.cpu_count() or 1
+    ext, dtype, box, _, desc = CONFIGS[cfg]
+    for _ in range(args.warmup):
+        cpu_sample(cfg, args.route, nthreads, planes=args.cpu_planes)
+    vals, shape = [], None
+    for _ in range(args.steps):
+        v, shape, _ = cpu_sample(cfg, args.route, nthreads, planes=args.cpu_planes)
+        vals.append(v)
+    value = statistics.median(vals)
+    n_step = int(np.prod(shape))
+    line = {
+        "impl": "reference", "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world,
+        "steps": args.steps, "warmup": args.warmup, "ms_per_step": n_step / value * 1e3,
+        "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": _dt(dtype),
+        "data": "synthetic",
+        "config": {"workload": cfg, "description": desc, "extents": list(ext), "box": list(box),
+                   "route": args.route},
+        "cpu_baseline": {"value": value, "unit": UNIT, "cores": nthreads, "kind": "port",
+                         "sample": f"{args.route} on the first {shape[0]} planes "
+                                   f"({'x'.join(map(str, shape))}) of the workload, "
+                                   f"oracle/exsum_oracle.c with {nthreads} OpenMP threads"},
+        "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+    }
+    print(json.dumps(line), flush=True)
+
+
+def _dt(dtype):
+    return {"float32": "f32", "float64": "f64", "int64": "int64"}[dtype]
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=10)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", default="b200", choices=["b200", "reference"])
+    ap.add_argument("--route", default="box-complement", choices=["box-complement", "bdbsc", "bdbs"])
+    ap.add_argument("--config", default="c4", choices=sorted(CONFIGS))
+    ap.add_argument("--cpu-planes", type=int, default=64)
+    ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--no-cpu", action="store_true")
+    args = ap.parse_args()
+
+    rank = int(os.environ.get("RANK", "0"))
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    if args.impl == "reference":
+        return run_reference(args, rank, world)
+
+    import torch
+
+    import paper_2106_00124_b200 as ex
+    from paper_2106_00124_b200 import _native
+
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    torch.cuda.set_device(local)
+    dev = torch.device("cuda", local)
+    dist = None
+    if world > 1:
+        import torch.distributed as dist
+
+        dist.init_process_group("nccl", device_id=dev)
+    ext, dtype, box, _, desc = CONFIGS[args.config]
+    N = int(np.prod(ext))
+    es = 4 if dtype == "float32" else 8
+    ops = ops_for(ex, dtype, args.route)
+    fn = {"box-complement": ex.box_complement_excluded, "bdbsc": ex.bdbs_excluded,
+          "bdbs": ex.bdbs_included}[args.route]
+
+    if world > 1:
+        from paper_2106_00124_b200 import sharded
+
+        x = sharded.make_local_slab(lambda shape: make_input(args.config, dev, shape=shape),
+                                    ext, rank, world)
+        runner = sharded.ShardedRunner(args.route, ops, ext, box, rank, world, dev)
+        step = lambda: runner(x)  # noqa: E731
+    else:
+        x = make_input(args.config, dev)
+        t = ex.Tensor(ops, x)
+        step = lambda: fn(t, box)  # noqa: E731
+
+    stream = torch.cuda.current_stream(dev)
+    for _ in range(args.warmup):
+        out = step()
+    torch.cuda.synchronize(dev)
+    del out
+
+    # -- timed region: K steps, device events on the launching stream --------
+    _native.profile_enable(True)
+    starts = [torch.cuda.Event(enable_timing=True) for _ in range(args.steps)]
+    ends = [torch.cuda.Event(enable_timing=True) for _ in range(args.steps)]
+    launches = 0
+    if dist is not None:
+        dist.barrier()
+    torch.cuda.synchronize(dev)
+    with ClockSampler(local) as clocks:
+        for i in range(args.steps):
+            starts[i].record(stream)
+            out = step()
+            ends[i].record(stream)
+            launches += _native.last_launch_count()
+            del out
+        torch.cuda.synchronize(dev)
+    if dist is not None:
+        dist.barrier()
+    step_ms = [s.elapsed_time(e) for s, e in zip(starts, ends)]
+    prof = _native.profile_records()
+    _native.profile_enable(False)
+    total_ms = sum(step_ms)
+    if dist is not None:
+        tt = torch.tensor([total_ms], device=dev, dtype=torch.float64)
+        dist.all_reduce(tt, op=dist.ReduceOp.MAX)
+        total_ms = float(tt.item())
+    ms_per_step = total_ms / args.steps
+    value = N * args.steps / (total_ms / 1e3)
+
+    # -- roofline of the dominant kernel (per-launch events inside the region) --
+    peak, peak_kind = _peaks()
+    per = {}
+    for name, b, ms in prof:
+        d = per.setdefault(name, {"ms": 0.0, "bytes": 0.0, "launches": 0})
+        d["ms"] += ms
+        d["bytes"] += b
+        d["launches"] += 1
+    dom = max(per, key=lambda k: per[k]["ms"]) if per else None
+    kernels = {}
+    for name, d in per.items():
+        gbs = d["bytes"] / (d["ms"] / 1e3) / 1e9 if d["ms"] > 0 else 0.0
+        kernels[name] = {"launches": d["launches"], "avg_ms": d["ms"] / d["launches"],
+                         "bytes_per_launch": d["bytes"] / d["launches"], "GBps": gbs,
+                         "share_of_step": d["ms"] / total_ms if total_ms else None}
+    roofline = None
+    if dom is not None:
+        d = per[dom]
+        ach = d["bytes"] / (d["ms"] / 1e3) / 1e9
+        roofline = {"bound": "hbm", "kernel": dom, "achieved": ach, "peak": peak, "unit": "GB/s",
+                    "frac": ach / peak, "peak_source": peak_kind, "traffic": _ncu_traffic(dom)}
+    step_bytes = sum(d["bytes"] for d in per.values()) / max(args.steps, 1)
+    e2e_frac = 2 * N * es / (ms_per_step / 1e3) / 1e9 / peak
+
+    # -- other routes on the same array, for context (not the headline) -------
+    routes = {}
+    if world == 1:
+        for rname, rfn in (("bdbsc", ex.bdbs_excluded), ("bdbs", ex.bdbs_included),
+                           ("box-complement", ex.box_complement_excluded)):
+            if rname == args.route or (rname == "bdbsc" and not ops.has_inverse):
+                continue
+            rt = ex.Tensor(ops, x)
+            for _ in range(2):
+                rfn(rt, box)
+            torch.cuda.synchronize(dev)
+            a_ev, b_ev = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            a_ev.record(stream)
+            reps = 3
+            for _ in range(reps):
+                o = rfn(rt, box)
+                del o
+            b_ev.record(stream)
+            torch.cuda.synchronize(dev)
+            ms = a_ev.elapsed_time(b_ev) / reps
+            routes[rname] = {"ms_per_step": ms, "elements_per_s": N / (ms / 1e3)}
+
+    # -- end to end through the public API with host buffers ------------------
+    e2e = None
+    if not args.no_e2e and world == 1:
+        host_in = torch.empty(ext, dtype=x.dtype, pin_memory=True)
+        host_in.copy_(x)
+        host_out = torch.empty_like(host_in, pin_memory=True)
+        a_np, o_np = host_in.numpy(), host_out.numpy()
+        from paper_2106_00124_b200.routes import run_host
+
+        k = ex.normalize_box(ext, box)
+        dname = {"float32": "float32", "float64": "float64", "int64": "int64"}[dtype]
+        run_host(args.route, a_np, dname, ops.op, ext, k, out=o_np)  # warm-up (allocates the cache)
+        e_steps = max(1, min(args.steps, 3))
+        times = []
+        for _ in range(e_steps):
+            t0 = time.perf_counter()
+            r = run_host(args.route, a_np, dname, ops.op, ext, k, out=o_np)
+            times.append(time.perf_counter() - t0)
+            launches_e2e = _native.last_launch_count()
+        del r
+        _native.load().exsum_release_cache()
+        e2e = {"value": N / statistics.median(times), "unit": UNIT,
+               "h2d_bytes_per_step": N * es, "d2h_bytes_per_step": N * es,
+               "ms_per_step": statistics.median(times) * 1e3, "steps": e_steps,
+               "path": "exsum_run_host (pinned host in/out; H2D + compute + D2H per step)"}
+
+    cpu = None
+    if not args.no_cpu and rank == 0 and world == 1:
+        nthreads = os.cpu_count() or 1
+        v, shape, dt = cpu_sample(args.config, args.route, nthreads, planes=args.cpu_planes)
+        cpu = {"value": v, "unit": UNIT, "cores": nthreads, "kind": "port",
+               "sample": f"{args.route} on the first {shape[0]} planes ({'x'.join(map(str, shape))}) "
+                         f"of the workload, oracle/exsum_oracle.c, {nthreads} OpenMP threads, "
+                         f"{dt:.2f} s"}
+
+    if rank == 0:
+        line = {
+            "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
+            "warmup": args.warmup, "ms_per_step": ms_per_step, "higher_is_better": True,
+            "scaling": "strong" if world > 1 else "strong", "vs_baseline": None,
+            "dtype": _dt(dtype), "data": "synthetic",
+            "config": {"workload": args.config, "description": desc, "extents": list(ext),
+                       "box": list(box), "route": args.route, "operator": ops.name,
+                       "parallelism": f"axis0-shards{world}" if world > 1 else "single-gpu",
+                       "l2": "input 4 GiB >> 126 MB L2; no flush needed" if N * es > 2**30
+                       else "input smaller than 4x L2"},
+            "roofline": roofline,
+            "hbm_GBps_step": step_bytes / (ms_per_step / 1e3) / 1e9,
+            "e2e_fraction_of_peak": e2e_frac,
+            "kernels": kernels,
+            "routes": routes,
+            "gpu_launches": launches,
+            "clocks": clocks.summary(),
+            "e2e": e2e,
+            "cpu_baseline": cpu,
+        }
+        print(json.dumps(line), flush=True)
+    if dist is not None:
+        dist.destroy_process_group()
+
+
+def _ncu_traffic(kernel):
+    """dram bytes per launch of `kernel` from the committed ncu summary, if any."""
+    try:
+        with open(os.path.join(ROOT, "profiles", "ncu_traffic.json")) as f:
+            return json.load(f).get(kernel)
+    except Exception:
+        return None
+
+
+if __name__ == "__main__":
+    main()

@@ -1,0 +1,122 @@
+/*
+ * exsum_b200.h -- C ABI of the B200-native box-sum library (libexsum_b200.so).
+ *
+ * Drop-in boundary for the reference's hot path (arxiv 2106.00124 `exsum`
+ * package, /root/reference/pkg/src/exsum).  The reference is Python; its
+ * plug-in surface is the set of callables `fn(t: Tensor, box) -> Tensor`
+ * registered in bench.ALGORITHMS (bench.py:60-76) plus bdbs_1d (scan.py:53).
+ * Each entry point below replaces one of them; the Python host layer
+ * (paper_2106_00124_b200/) binds them with ctypes exactly as a maintainer of
+ * the reference would.
+ *
+ * Conventions:
+ *   - arrays are dense C-order (last axis contiguous), same
+ *     extents and dtype in and out; `in` is never written; out != in;
+ *   - box sides are clamped to the extents (tensor.py:32-48); windows are
+ *     forward, half-open, clipped at the end;
+ *   - work is stream-ordered on `stream` (a cudaStream_t; NULL = legacy
+ *     default stream); the call returns after enqueueing;
+ *   - no hidden device allocations on the device-pointer entry points: the
+ *     caller passes a workspace of exsum_workspace_bytes() bytes;
+ *   - no CPU fallback: an unsupported dtype/operator is EXSUM_ECONFIG.
+ *
+ * Return codes map onto the reference's exceptions (errors.py:8-22):
+ *   EXSUM_OK 0, EXSUM_EUSAGE 1 (UsageError: bad extents / box arity / k < 1),
+ *   EXSUM_ECONFIG 2 (ConfigurationError: e.g. weak route on max),
+ *   EXSUM_ECUDA 3 (CUDA runtime failure; see exsum_last_error()).
+ */
+#ifndef EXSUM_B200_H
+#define EXSUM_B200_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define EXSUM_ABI_VERSION 1
+
+/* element types (MonoidOps.dtype, monoid.py:40) */
+#define EXSUM_F32 0 /* add-f32 (test-side float32 FloatAddOps)      */
+#define EXSUM_F64 1 /* add-f64  FloatAddOps   monoid.py:167-204      */
+#define EXSUM_I64 2 /* add-i64 / max-i64      monoid.py:130-164,207-232 */
+
+/* operators (MonoidOps.combine) */
+#define EXSUM_ADD 0
+#define EXSUM_MAX 1
+
+/* routes (bench.ALGORITHMS names, bench.py:60-76) */
+#define EXSUM_ROUTE_BDBS 0           /* "bdbs"           included.py:124-129 */
+#define EXSUM_ROUTE_BDBSC 1          /* "bdbsc"          excluded.py:88-90   */
+#define EXSUM_ROUTE_BOX_COMPLEMENT 2 /* "box-complement" excluded.py:129-159 */
+
+#define EXSUM_OK 0
+#define EXSUM_EUSAGE 1
+#define EXSUM_ECONFIG 2
+#define EXSUM_ECUDA 3
+
+#define EXSUM_MAX_DIMS 32
+
+/* ABI version of the loaded library (== EXSUM_ABI_VERSION). */
+int exsum_abi_version(void);
+
+/* Message for the last non-zero return on this thread ("" if none). */
+const char *exsum_last_error(void);
+
+/* Workspace bytes the route needs for these extents/box (validated like the
+ * route itself).  Replaces the reference's hidden allocations
+ * (alloc.new_array, alloc.py:63-65; tensor.py:91-114; scan.py:70). */
+int exsum_workspace_bytes(int route, int dtype, int op, int d, const int64_t *ext,
+                          const int64_t *box, size_t *bytes);
+
+/* Strong included sum, any monoid.  Replaces bdbs_included(t, box)
+ * (included.py:124-129); bdbs_1d(ops, values, k) (scan.py:53-58) is d == 1. */
+int exsum_bdbs_included(const void *in, void *out, int dtype, int op, int d,
+                        const int64_t *ext, const int64_t *box, void *ws, size_t ws_bytes,
+                        void *stream);
+
+/* Weak excluded sum (total (-) included), invertible monoids only (add).
+ * Replaces bdbs_excluded(t, box) (excluded.py:88-90, 72-75). */
+int exsum_bdbsc_excluded(const void *in, void *out, int dtype, int op, int d,
+                         const int64_t *ext, const int64_t *box, void *ws, size_t ws_bytes,
+                         void *stream);
+
+/* Strong excluded sum, any monoid.  Replaces box_complement_excluded(t, box)
+ * (excluded.py:129-159). */
+int exsum_box_complement_excluded(const void *in, void *out, int dtype, int op, int d,
+                                  const int64_t *ext, const int64_t *box, void *ws,
+                                  size_t ws_bytes, void *stream);
+
+/* One windowed pass along `axis` (out-of-place).  Replaces
+ * windowed_sum_axis(ops, view, k, axis) (scan.py:61-102) on a dense array. */
+int exsum_windowed_pass(const void *in, void *out, int dtype, int op, int d,
+                        const int64_t *ext, int axis, int64_t k, void *stream);
+
+/* Host-buffer convenience: copies h_in to the device, runs `route`, copies
+ * the result to h_out and synchronizes.  Device buffers are cached per
+ * device between calls.  This is the call a host-side plug-in makes
+ * (AlgorithmInfo.run with numpy data, bench.py:54-57). */
+int exsum_run_host(int route, const void *h_in, void *h_out, int dtype, int op, int d,
+                   const int64_t *ext, const int64_t *box);
+
+/* Release the device buffers cached by exsum_run_host. */
+int exsum_release_cache(void);
+
+/* Number of kernels the last successful call on this thread launched
+ * (instrumentation for bench.py's gpu_launches). */
+int exsum_last_launch_count(void);
+
+/* Per-kernel CUDA-event profiling of the calls made on this thread (for
+ * bench.py's roofline): enable (clears old records), run, synchronize, then
+ * read each launch's name, algorithmic bytes (compulsory reads + writes) and
+ * device time in milliseconds. */
+int exsum_profile_enable(int on);
+int exsum_profile_count(void);
+int exsum_profile_get(int i, char *name, int name_len, double *bytes, float *ms);
+
+#ifdef __cplusplus
+}
+#endif
+
+#endif /* EXSUM_B200_H */

@@ -1,0 +1,50 @@
+"""B200-native box sums (arXiv 2106.00124): drop-in for the reference hot path.
+
+Public names mirror the reference package ``exsum`` (pkg/src/exsum/__init__.py)
+for the accelerated path: ``bdbs_included``, ``bdbs_excluded``,
+``box_complement_excluded``, ``bdbs_1d``, ``windowed_sum_axis``, ``Tensor``,
+the monoids and the error types, plus the ``ALGORITHMS`` registry.  All
+arithmetic runs in hand-written sm_100a CUDA kernels (``csrc/``) behind the C
+ABI in ``include/exsum_b200.h``; there is no CPU fallback.
+"""
+
+from .errors import (
+    ConfigurationError,
+    DeviceError,
+    ExsumError,
+    UsageError,
+    VerificationError,
+)
+from .monoid import (
+    MONOID_CHOICES,
+    Float32AddOps,
+    FloatAddOps,
+    IntAddOps,
+    IntMaxOps,
+    MonoidOps,
+    resolve_monoid,
+)
+from .routes import (
+    ALGORITHMS,
+    AlgorithmInfo,
+    bdbs_1d,
+    bdbs_excluded,
+    bdbs_included,
+    box_complement_excluded,
+    check_algorithm_config,
+    register_with_reference,
+    resolve_algorithm,
+    windowed_sum_axis,
+)
+from .tensor import Tensor, crop_to, normalize_box, pad_to_box_multiple, validate_extents
+
+__version__ = "0.1.0"
+
+__all__ = [
+    "ALGORITHMS", "AlgorithmInfo", "ConfigurationError", "DeviceError", "ExsumError",
+    "Float32AddOps", "FloatAddOps", "IntAddOps", "IntMaxOps", "MONOID_CHOICES", "MonoidOps",
+    "Tensor", "UsageError", "VerificationError", "bdbs_1d", "bdbs_excluded", "bdbs_included",
+    "box_complement_excluded", "check_algorithm_config", "crop_to", "normalize_box",
+    "pad_to_box_multiple", "register_with_reference", "resolve_algorithm", "resolve_monoid",
+    "validate_extents", "windowed_sum_axis",
+]

@@ -1,0 +1,488 @@
+// exsum_capi.cu -- C ABI (include/exsum_b200.h) and route orchestration.
+//
+// Routes (reference pkg/src/exsum):
+//   bdbs            included.py:124-129   one windowed pass per axis, axes in
+//                                          order 0..d-1 (bit-exact association)
+//   bdbsc           excluded.py:88-90     total fold + bdbs, complement fused
+//                                          into the last pass's stores
+//   box-complement  excluded.py:129-159   slab decomposition, peeling the LAST
+//                                          axis first (see below)
+//
+// Box-complement order.  The reference peels dimension 0 first: round i adds
+// the "below"/"above" slabs of dimension i on the reduced slice.  The slab
+// decomposition is valid in any dimension order (the complement of a box is
+// the disjoint union, over the peeled dimension, of {outside the window in
+// that dimension, inside the box in the not-yet-peeled ones} plus the
+// complement in the remaining dimensions of the reduction), so this build
+// peels the contiguous last axis first:
+//     BC(A, k) = E_{d-1}(W) (+) bcast_rows( BC(R, k[:-1]) )
+//     W = windowed passes of A along axes 0..d-2 (same kernels as bdbs)
+//     R = (+)-reduction of A over the last axis
+//     E_{d-1}(W)[.., x] = P(W)[.., x-1] (+) S(W)[.., x+k_{d-1}]  (full-row scans)
+// so the full-array rounds are d-1 streaming passes plus one row kernel, and
+// the recursion runs on arrays n_{d-1} times smaller.  Integer + and max are
+// exact, so the result is bit-identical to the reference; float + agrees to
+// the reassociation bound.
+#include <cuda_runtime.h>
+
+#include <stdio.h>
+
+#include <mutex>
+#include <string>
+#include <vector>
+
+#include "../../include/exsum_b200.h"
+#include "exsum_launch.h"
+
+using namespace exsum;
+
+namespace {
+
+thread_local std::string g_err;
+
+int fail(int code, const std::string& msg) {
+  g_err = msg;
+  return code;
+}
+
+int cuda_check(const char* what) {
+  cudaError_t e = cudaGetLastError();
+  if (e != cudaSuccess) return fail(EXSUM_ECUDA, std::string(what) + ": " + cudaGetErrorString(e));
+  return EXSUM_OK;
+}
+
+// Optional per-launch CUDA-event profiler (exsum_profile_*): bench.py uses it
+// to time each kernel on its own stream inside the timed region and to pair
+// it with the kernel's algorithmic bytes for the roofline.
+struct ProfRec {
+  const char* name;
+  double bytes;
+  cudaEvent_t a, b;
+};
+struct Profiler {
+  bool on = false;
+  std::vector<ProfRec> recs;
+  std::vector<cudaEvent_t> pool;
+  size_t used = 0;
+  cudaEvent_t ev() {
+    if (used == pool.size()) {
+      cudaEvent_t e;
+      cudaEventCreate(&e);
+      pool.push_back(e);
+    }
+    return pool[used++];
+  }
+};
+thread_local Profiler g_prof;
+
+struct ProfScope {
+  cudaStream_t st;
+  bool on;
+  ProfScope(const char* name, double bytes, cudaStream_t s) : st(s), on(g_prof.on) {
+    if (!on) return;
+    ProfRec r{name, bytes, g_prof.ev(), g_prof.ev()};
+    cudaEventRecord(r.a, st);
+    g_prof.recs.push_back(r);
+  }
+  ~ProfScope() {
+    if (on) cudaEventRecord(g_prof.recs.back().b, st);
+  }
+};
+
+struct Shape {
+  int d = 0;
+  int64_t ext[EXSUM_MAX_DIMS];
+  int64_t k[EXSUM_MAX_DIMS];
+  int64_t N = 1;
+};
+
+// tensor.py:20-48 (validate_extents + normalize_box): arity, n >= 1, k >= 1,
+// k clamped to n.
+int normalize(int d, const int64_t* ext, const int64_t* box, Shape* s) {
+  if (d < 1 || d > EXSUM_MAX_DIMS) return fail(EXSUM_EUSAGE, "extents must have 1..32 dimensions");
+  if (!ext || !box) return fail(EXSUM_EUSAGE, "null extents or box");
+  s->d = d;
+  s->N = 1;
+  for (int i = 0; i < d; ++i) {
+    if (ext[i] < 1) return fail(EXSUM_EUSAGE, "every extent must be >= 1");
+    if (box[i] < 1) return fail(EXSUM_EUSAGE, "every box side must be >= 1");
+    s->ext[i] = ext[i];
+    s->k[i] = box[i] < ext[i] ? box[i] : ext[i];
+    s->N *= ext[i];
+  }
+  return EXSUM_OK;
+}
+
+int check_types(int dtype, int op) {
+  if (dtype != EXSUM_F32 && dtype != EXSUM_F64 && dtype != EXSUM_I64)
+    return fail(EXSUM_ECONFIG, "unsupported dtype (float32, float64, int64)");
+  if (op != EXSUM_ADD && op != EXSUM_MAX) return fail(EXSUM_ECONFIG, "unsupported operator");
+  if (op == EXSUM_MAX && dtype != EXSUM_I64)
+    return fail(EXSUM_ECONFIG, "max is provided for int64 only (max-i64, monoid.py:207-232)");
+  return EXSUM_OK;
+}
+
+// Bump allocator over the caller's workspace; base == nullptr sizes only.
+struct Arena {
+  char* base;
+  size_t off = 0;
+  explicit Arena(void* b) : base((char*)b) {}
+  void* take(size_t bytes) {
+    off = (off + 255) & ~(size_t)255;
+    void* p = base ? base + off : nullptr;
+    off += bytes;
+    return p;
+  }
+};
+
+int64_t prod(const int64_t* e, int lo, int hi) {
+  int64_t p = 1;
+  for (int i = lo; i < hi; ++i) p *= e[i];
+  return p;
+}
+
+// Windowed passes along the listed axes, ending in `final_dst`; intermediate
+// results alternate between final_dst and `other` (both != src).
+struct PassPlan {
+  int axes[EXSUM_MAX_DIMS];
+  int count = 0;
+};
+
+PassPlan plan_passes(const Shape& s, int upto) {
+  PassPlan p;
+  for (int a = 0; a < upto; ++a)
+    if (s.k[a] > 1) p.axes[p.count++] = a;
+  return p;
+}
+
+int run_passes(const Shape& s, const PassPlan& p, int dtype, int op, const void* src,
+               void* final_dst, void* other, const void* epi_total, cudaStream_t st,
+               int* launches) {
+  const void* cur = src;
+  for (int i = 0; i < p.count; ++i) {
+    const int a = p.axes[i];
+    const int remaining = p.count - 1 - i;
+    void* dst = (remaining % 2 == 0) ? final_dst : other;
+    const bool last = i == p.count - 1;
+    const size_t es = dtype_size(dtype);
+    ProfScope ps(a == s.d - 1 ? "pass_rows" : "pass_strided", 2.0 * (double)s.N * es, st);
+    int rc = launch_pass(dtype, op, cur, dst, prod(s.ext, 0, a), s.ext[a], prod(s.ext, a + 1, s.d),
+                         s.k[a], last ? epi_total : nullptr, st);
+    if (rc < 0) return fail(EXSUM_ECONFIG, "no kernel for this dtype/operator");
+    *launches += rc;
+    cur = dst;
+  }
+  return EXSUM_OK;
+}
+
+// ------------------------------------------------------------------ routes --
+
+int route_bdbs(const Shape& s, int dtype, int op, const void* in, void* out, Arena& ar,
+               bool complement, cudaStream_t st, int* launches) {
+  const size_t es = dtype_size(dtype);
+  PassPlan p = plan_passes(s, s.d);
+  void* total = nullptr;
+  if (complement) {
+    void* partials = ar.take((size_t)reduce_partials_count() * 8);
+    total = ar.take(8);
+    if (ar.base) {
+      ProfScope ps("total", (double)s.N * es, st);
+      *launches += launch_total(dtype, op, in, s.N, partials, total, st);
+    }
+  }
+  void* other = p.count >= 2 ? ar.take((size_t)s.N * es) : nullptr;
+  if (!ar.base) return EXSUM_OK;
+  if (p.count == 0) {
+    ProfScope ps(complement ? "complement" : "copy", 2.0 * (double)s.N * es, st);
+    if (complement) {
+      *launches += launch_complement(dtype, in, out, s.N, total, st);
+    } else {
+      cudaMemcpyAsync(out, in, (size_t)s.N * es, cudaMemcpyDeviceToDevice, st);
+    }
+    return EXSUM_OK;
+  }
+  return run_passes(s, p, dtype, op, in, out, other, total, st, launches);
+}
+
+// BC(src) -> dst, peeling the last axis (see file header).
+int route_box_complement(const Shape& s, int dtype, int op, const void* src, void* dst,
+                         Arena& ar, cudaStream_t st, int* launches) {
+  const size_t es = dtype_size(dtype);
+  const int d = s.d;
+  const int64_t n = s.ext[d - 1];
+  const int64_t rows = s.N / n;
+  if (d == 1) {
+    void* scratch = ar.take(excl_rows_scratch_elems(dtype, 1, n) * es);
+    if (ar.base) {
+      ProfScope ps("excl_rows", 2.0 * (double)n * es, st);
+      *launches += launch_excl_rows(dtype, op, src, dst, nullptr, 1, n, s.k[0], scratch, st);
+    }
+    return EXSUM_OK;
+  }
+  // R = reduction over the last axis; T = BC(R, k[:-1])
+  void* R = ar.take((size_t)rows * es);
+  void* T = ar.take((size_t)rows * es);
+  if (ar.base) {
+    ProfScope ps("row_reduce", (double)(s.N + rows) * es, st);
+    *launches += launch_row_reduce(dtype, op, src, R, rows, n, st);
+  }
+  Shape t;
+  t.d = d - 1;
+  t.N = rows;
+  for (int i = 0; i < d - 1; ++i) {
+    t.ext[i] = s.ext[i];
+    t.k[i] = s.k[i];
+  }
+  int rc = route_box_complement(t, dtype, op, R, T, ar, st, launches);
+  if (rc) return rc;
+  // W = windowed passes along axes 0..d-2 (never aliases dst)
+  PassPlan p = plan_passes(s, d - 1);
+  const void* W = src;
+  if (p.count > 0) {
+    void* wbuf = ar.take((size_t)s.N * es);
+    if (ar.base) {
+      rc = run_passes(s, p, dtype, op, src, wbuf, dst, nullptr, st, launches);
+      if (rc) return rc;
+    }
+    W = wbuf;
+  }
+  void* scratch = ar.take(excl_rows_scratch_elems(dtype, rows, n) * es);
+  if (ar.base) {
+    ProfScope ps("excl_rows", (double)(2 * s.N + rows) * es, st);
+    *launches += launch_excl_rows(dtype, op, W, dst, T, rows, n, s.k[d - 1], scratch, st);
+  }
+  return EXSUM_OK;
+}
+
+int dispatch(int route, const Shape& s, int dtype, int op, const void* in, void* out, Arena& ar,
+             cudaStream_t st, int* launches) {
+  switch (route) {
+    case EXSUM_ROUTE_BDBS:
+      return route_bdbs(s, dtype, op, in, out, ar, false, st, launches);
+    case EXSUM_ROUTE_BDBSC:
+      return route_bdbs(s, dtype, op, in, out, ar, true, st, launches);
+    case EXSUM_ROUTE_BOX_COMPLEMENT:
+      return route_box_complement(s, dtype, op, in, out, ar, st, launches);
+  }
+  return fail(EXSUM_ECONFIG, "unknown route");
+}
+
+int validate(int route, int dtype, int op, int d, const int64_t* ext, const int64_t* box,
+             Shape* s) {
+  int rc = check_types(dtype, op);
+  if (rc) return rc;
+  if (route < 0 || route > 2) return fail(EXSUM_ECONFIG, "unknown route");
+  // bench.check_algorithm_config (bench.py:88-100): weak route needs an inverse
+  if (route == EXSUM_ROUTE_BDBSC && op == EXSUM_MAX)
+    return fail(EXSUM_ECONFIG, "algorithm 'bdbsc' requires an invertible monoid, but 'max-i64' has no inverse");
+  return normalize(d, ext, box, s);
+}
+
+thread_local int g_last_launches = 0;
+
+int run_device(int route, const void* in, void* out, int dtype, int op, int d, const int64_t* ext,
+               const int64_t* box, void* ws, size_t ws_bytes, void* stream) {
+  g_err.clear();
+  Shape s;
+  int rc = validate(route, dtype, op, d, ext, box, &s);
+  if (rc) return rc;
+  if (!in || !out) return fail(EXSUM_EUSAGE, "null array pointer");
+  if (in == out) return fail(EXSUM_EUSAGE, "out must not alias in");
+  Arena sizing(nullptr);
+  int launches = 0;
+  rc = dispatch(route, s, dtype, op, in, out, sizing, (cudaStream_t)stream, &launches);
+  if (rc) return rc;
+  if (sizing.off > 0 && (ws == nullptr || ws_bytes < sizing.off))
+    return fail(EXSUM_EUSAGE, "workspace too small (see exsum_workspace_bytes)");
+  Arena ar(ws);
+  launches = 0;
+  rc = dispatch(route, s, dtype, op, in, out, ar, (cudaStream_t)stream, &launches);
+  if (rc) return rc;
+  g_last_launches = launches;
+  return cuda_check("kernel launch");
+}
+
+// ----------------------------------------------------- host buffer cache --
+struct DevBuf {
+  void* p = nullptr;
+  size_t cap = 0;
+  int reserve(size_t bytes) {
+    if (bytes <= cap) return 0;
+    if (p) cudaFree(p);
+    p = nullptr;
+    cap = 0;
+    if (cudaMalloc(&p, bytes) != cudaSuccess) return -1;
+    cap = bytes;
+    return 0;
+  }
+  void release() {
+    if (p) cudaFree(p);
+    p = nullptr;
+    cap = 0;
+  }
+};
+
+struct HostCache {
+  std::mutex mu;
+  std::vector<int> dev;
+  std::vector<DevBuf> in, out, ws;
+  std::vector<cudaStream_t> stream;
+};
+
+HostCache& host_cache() {
+  static HostCache c;
+  return c;
+}
+
+}  // namespace
+
+extern "C" {
+
+int exsum_abi_version(void) { return EXSUM_ABI_VERSION; }
+
+const char* exsum_last_error(void) { return g_err.c_str(); }
+
+int exsum_last_launch_count(void) { return g_last_launches; }
+
+int exsum_workspace_bytes(int route, int dtype, int op, int d, const int64_t* ext,
+                          const int64_t* box, size_t* bytes) {
+  g_err.clear();
+  Shape s;
+  int rc = validate(route, dtype, op, d, ext, box, &s);
+  if (rc) return rc;
+  Arena sizing(nullptr);
+  int launches = 0;
+  rc = dispatch(route, s, dtype, op, (const void*)1, (void*)2, sizing, nullptr, &launches);
+  if (rc) return rc;
+  if (bytes) *bytes = sizing.off;
+  return EXSUM_OK;
+}
+
+int exsum_bdbs_included(const void* in, void* out, int dtype, int op, int d, const int64_t* ext,
+                        const int64_t* box, void* ws, size_t ws_bytes, void* stream) {
+  return run_device(EXSUM_ROUTE_BDBS, in, out, dtype, op, d, ext, box, ws, ws_bytes, stream);
+}
+
+int exsum_bdbsc_excluded(const void* in, void* out, int dtype, int op, int d, const int64_t* ext,
+                         const int64_t* box, void* ws, size_t ws_bytes, void* stream) {
+  return run_device(EXSUM_ROUTE_BDBSC, in, out, dtype, op, d, ext, box, ws, ws_bytes, stream);
+}
+
+int exsum_box_complement_excluded(const void* in, void* out, int dtype, int op, int d,
+                                  const int64_t* ext, const int64_t* box, void* ws,
+                                  size_t ws_bytes, void* stream) {
+  return run_device(EXSUM_ROUTE_BOX_COMPLEMENT, in, out, dtype, op, d, ext, box, ws, ws_bytes,
+                    stream);
+}
+
+int exsum_windowed_pass(const void* in, void* out, int dtype, int op, int d, const int64_t* ext,
+                        int axis, int64_t k, void* stream) {
+  g_err.clear();
+  int rc = check_types(dtype, op);
+  if (rc) return rc;
+  if (d < 1 || d > EXSUM_MAX_DIMS || !ext) return fail(EXSUM_EUSAGE, "bad extents");
+  if (axis < 0 || axis >= d) return fail(EXSUM_EUSAGE, "axis out of range");
+  if (k < 1) return fail(EXSUM_EUSAGE, "window must be >= 1");
+  if (!in || !out || in == out) return fail(EXSUM_EUSAGE, "need distinct in/out");
+  for (int i = 0; i < d; ++i)
+    if (ext[i] < 1) return fail(EXSUM_EUSAGE, "every extent must be >= 1");
+  const int64_t n = ext[axis];
+  if (k > n) k = n;
+  cudaStream_t st = (cudaStream_t)stream;
+  if (k == 1) {
+    cudaMemcpyAsync(out, in, (size_t)prod(ext, 0, d) * dtype_size(dtype), cudaMemcpyDeviceToDevice, st);
+    g_last_launches = 0;
+  } else {
+    rc = launch_pass(dtype, op, in, out, prod(ext, 0, axis), n, prod(ext, axis + 1, d), k, nullptr, st);
+    if (rc < 0) return fail(EXSUM_ECONFIG, "no kernel for this dtype/operator");
+    g_last_launches = rc;
+  }
+  return cuda_check("kernel launch");
+}
+
+int exsum_run_host(int route, const void* h_in, void* h_out, int dtype, int op, int d,
+                   const int64_t* ext, const int64_t* box) {
+  g_err.clear();
+  Shape s;
+  int rc = validate(route, dtype, op, d, ext, box, &s);
+  if (rc) return rc;
+  if (!h_in || !h_out) return fail(EXSUM_EUSAGE, "null host pointer");
+  size_t ws_bytes = 0;
+  rc = exsum_workspace_bytes(route, dtype, op, d, ext, box, &ws_bytes);
+  if (rc) return rc;
+  int dev = 0;
+  if (cudaGetDevice(&dev) != cudaSuccess) return cuda_check("cudaGetDevice");
+  HostCache& c = host_cache();
+  std::lock_guard<std::mutex> lock(c.mu);
+  size_t slot = 0;
+  while (slot < c.dev.size() && c.dev[slot] != dev) ++slot;
+  if (slot == c.dev.size()) {
+    c.dev.push_back(dev);
+    c.in.emplace_back();
+    c.out.emplace_back();
+    c.ws.emplace_back();
+    cudaStream_t st;
+    if (cudaStreamCreateWithFlags(&st, cudaStreamNonBlocking) != cudaSuccess)
+      return cuda_check("cudaStreamCreate");
+    c.stream.push_back(st);
+  }
+  const size_t bytes = (size_t)s.N * dtype_size(dtype);
+  if (c.in[slot].reserve(bytes) || c.out[slot].reserve(bytes) ||
+      c.ws[slot].reserve(ws_bytes > 0 ? ws_bytes : 256))
+    return fail(EXSUM_ECUDA, "cudaMalloc failed for host-path buffers");
+  cudaStream_t st = c.stream[slot];
+  cudaMemcpyAsync(c.in[slot].p, h_in, bytes, cudaMemcpyHostToDevice, st);
+  rc = run_device(route, c.in[slot].p, c.out[slot].p, dtype, op, d, ext, box, c.ws[slot].p,
+                  c.ws[slot].cap, st);
+  if (rc) return rc;
+  cudaMemcpyAsync(h_out, c.out[slot].p, bytes, cudaMemcpyDeviceToHost, st);
+  if (cudaStreamSynchronize(st) != cudaSuccess) return cuda_check("cudaStreamSynchronize");
+  return cuda_check("host path");
+}
+
+int exsum_profile_enable(int on) {
+  g_prof.on = on != 0;
+  g_prof.recs.clear();
+  g_prof.used = 0;
+  return EXSUM_OK;
+}
+
+int exsum_profile_count(void) { return (int)g_prof.recs.size(); }
+
+int exsum_profile_get(int i, char* name, int name_len, double* bytes, float* ms) {
+  if (i < 0 || i >= (int)g_prof.recs.size()) return fail(EXSUM_EUSAGE, "profile index out of range");
+  const ProfRec& r = g_prof.recs[i];
+  if (name && name_len > 0) {
+    snprintf(name, (size_t)name_len, "%s", r.name);
+  }
+  if (bytes) *bytes = r.bytes;
+  if (ms) {
+    float v = 0.f;
+    if (cudaEventElapsedTime(&v, r.a, r.b) != cudaSuccess) return cuda_check("cudaEventElapsedTime");
+    *ms = v;
+  }
+  return EXSUM_OK;
+}
+
+int exsum_release_cache(void) {
+  HostCache& c = host_cache();
+  std::lock_guard<std::mutex> lock(c.mu);
+  int cur = 0;
+  cudaGetDevice(&cur);
+  for (size_t i = 0; i < c.dev.size(); ++i) {
+    cudaSetDevice(c.dev[i]);
+    c.in[i].release();
+    c.out[i].release();
+    c.ws[i].release();
+    cudaStreamDestroy(c.stream[i]);
+  }
+  cudaSetDevice(cur);
+  c.dev.clear();
+  c.in.clear();
+  c.out.clear();
+  c.ws.clear();
+  c.stream.clear();
+  return EXSUM_OK;
+}
+
+}  // extern "C"

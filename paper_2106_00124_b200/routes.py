@@ -1,0 +1,228 @@
+"""The hot-path entry points, with the reference's signatures.
+
+=============================  ==========================================
+this module                    reference (pkg/src/exsum)
+=============================  ==========================================
+bdbs_included(t, box)          included.py:124-129
+bdbs_excluded(t, box)          excluded.py:88-90 (+ _complement :72-75)
+box_complement_excluded(t,box) excluded.py:129-159
+bdbs_1d(ops, values, k)        scan.py:53-58
+windowed_sum_axis(ops,v,k,ax)  scan.py:61-102 (in place on ``v``)
+ALGORITHMS / AlgorithmInfo     bench.py:45-100 (the plug-in registry)
+=============================  ==========================================
+
+Every call validates exactly like the reference (``normalize_box``; a weak
+route on a monoid without inverse raises ``ConfigurationError`` before any
+work, like bench.check_algorithm_config) and then runs on the B200 through
+the C ABI.  Data placement decides the path:
+
+* ``t.data`` is a CUDA ``torch.Tensor``: device pointers go straight to the
+  stream-ordered entry points on ``torch.cuda.current_stream()``; the result is
+  a new CUDA tensor (no host copies).
+* ``t.data`` is a numpy array (the reference's own Tensor, for instance):
+  ``exsum_run_host`` copies it to HBM, computes, and copies the result back.
+
+The result is a new tensor carrying the caller's ``t.ops`` (bench.py:221,233
+re-wraps results with ``with_ops``), of the caller's Tensor class.
+"""
+
+from __future__ import annotations
+
+from dataclasses import dataclass
+
+import numpy as np
+
+from . import _native
+from .errors import ConfigurationError, UsageError
+from .monoid import device_operator
+from .tensor import Tensor, is_torch, normalize_box, np_dtype_of
+
+_DT_NAME = {np.dtype(np.float32): "float32", np.dtype(np.float64): "float64",
+            np.dtype(np.int64): "int64"}
+
+
+def _prepare(t, box, route):
+    dtype, op, has_inverse = device_operator(t.ops)
+    if route == "bdbsc" and not has_inverse:
+        raise ConfigurationError(
+            f"algorithm 'bdbsc' requires an invertible monoid, but {t.ops.name!r} has no inverse"
+        )
+    data = t.data
+    ext = tuple(int(v) for v in data.shape)
+    k = normalize_box(ext, box)
+    if np_dtype_of(data) != dtype:
+        raise UsageError(f"dtype {np_dtype_of(data)} does not match monoid {t.ops.name}")
+    return _DT_NAME[dtype], op, ext, k
+
+
+def _rewrap(t, out):
+    try:
+        return type(t)(t.ops, out)
+    except Exception:
+        return Tensor(t.ops, out)
+
+
+def run_device(route: str, x, dtype: str, op: str, ext, k, out=None):
+    """Run ``route`` on a CUDA torch tensor; returns the output tensor."""
+    import torch
+
+    if not x.is_cuda:
+        raise UsageError("run_device needs a CUDA tensor")
+    x = x.contiguous()
+    if out is None:
+        out = torch.empty_like(x)
+    L = _native.load()
+    ws_bytes = _native.workspace_bytes(route, dtype, op, ext, k)
+    with torch.cuda.device(x.device):
+        ws = torch.empty(max(ws_bytes, 1), dtype=torch.uint8, device=x.device)
+        stream = torch.cuda.current_stream(x.device).cuda_stream
+        fn = {
+            "bdbs": L.exsum_bdbs_included,
+            "bdbsc": L.exsum_bdbsc_excluded,
+            "box-complement": L.exsum_box_complement_excluded,
+        }[route]
+        _native.check(fn(x.data_ptr(), out.data_ptr(), _native.DTYPE[dtype], _native.OP[op],
+                         len(ext), _native.i64_array(ext), _native.i64_array(k),
+                         ws.data_ptr(), ws_bytes, stream))
+    return out
+
+
+def run_host(route: str, a: np.ndarray, dtype: str, op: str, ext, k, out=None) -> np.ndarray:
+    """Run ``route`` on a host array through exsum_run_host (H2D, compute, D2H).
+
+    ``out`` (optional) receives the result; pass page-locked buffers (e.g. a
+    numpy view of a pinned torch tensor) for full PCIe bandwidth."""
+    a = np.ascontiguousarray(a)
+    if out is None:
+        out = np.empty_like(a)
+    elif out.shape != a.shape or out.dtype != a.dtype or not out.flags.c_contiguous:
+        raise UsageError("out must be a C-contiguous array of the input's shape and dtype")
+    L = _native.load()
+    _native.check(L.exsum_run_host(_native.ROUTE[route], a.ctypes.data, out.ctypes.data,
+                                   _native.DTYPE[dtype], _native.OP[op], len(ext),
+                                   _native.i64_array(ext), _native.i64_array(k)))
+    return out
+
+
+def _route(route, t, box):
+    dtype, op, ext, k = _prepare(t, box, route)
+    data = t.data
+    if is_torch(data):
+        if data.is_cuda:
+            return _rewrap(t, run_device(route, data, dtype, op, ext, k))
+        out = run_host(route, data.numpy(), dtype, op, ext, k)
+        import torch
+
+        return _rewrap(t, torch.from_numpy(out))
+    return _rewrap(t, run_host(route, np.asarray(data), dtype, op, ext, k))
+
+
+def bdbs_included(t, box):
+    """Strong included sum: out[x] = (+) over the clipped box [x, x+k)."""
+    return _route("bdbs", t, box)
+
+
+def bdbs_excluded(t, box):
+    """Weak excluded sum: total (-) included (needs an invertible monoid)."""
+    return _route("bdbsc", t, box)
+
+
+def box_complement_excluded(t, box):
+    """Strong excluded sum over the complement of the clipped box (any monoid)."""
+    return _route("box-complement", t, box)
+
+
+def bdbs_1d(ops, values, k):
+    """Windowed sums of a 1-D sequence: out[x] = fold(values[x : x+k])."""
+    dtype, op, _ = device_operator(ops)
+    arr = np.array(values, dtype=dtype).reshape(-1)
+    (kk,) = normalize_box(arr.shape, (k,))
+    return run_host("bdbs", arr, _DT_NAME[dtype], op, arr.shape, (kk,))
+
+
+def windowed_sum_axis(ops, view, k, axis):
+    """In-place windowed sums along ``axis`` of ``view`` (scan.py:61-102)."""
+    dtype, op, _ = device_operator(ops)
+    ext = tuple(int(v) for v in view.shape)
+    if not 0 <= axis < len(ext):
+        raise UsageError(f"axis {axis} out of range for {len(ext)}-D view")
+    if int(k) < 1:
+        raise UsageError(f"every box side must be >= 1, got {k}")
+    if min(ext, default=1) == 0 or int(k) == 1:
+        return
+    box = tuple(int(k) if i == axis else 1 for i in range(len(ext)))
+    t = Tensor(_OpsShim(ops), view.contiguous() if is_torch(view) else np.ascontiguousarray(view))
+    res = bdbs_included(t, box)
+    if is_torch(view):
+        view.copy_(res.data)
+    else:
+        view[...] = res.data
+
+
+class _OpsShim:
+    def __init__(self, ops):
+        self.inner = ops
+        self.name = getattr(ops, "name", "?")
+        self.dtype = ops.dtype
+        self.identity = getattr(ops, "identity", 0)
+
+
+# -- the plug-in registry (bench.py:45-100) -------------------------------------
+
+
+@dataclass(frozen=True)
+class AlgorithmInfo:
+    name: str
+    fn: object
+    kind: str  # "included" or "excluded"
+    needs_inverse: bool
+    dims: object = None
+    cache_arg: str = ""
+
+    def run(self, t, box, cache: int = 1):
+        if self.cache_arg:
+            return self.fn(t, box, **{self.cache_arg: cache})
+        return self.fn(t, box)
+
+
+ALGORITHMS = {
+    info.name: info
+    for info in (
+        AlgorithmInfo("bdbs", bdbs_included, "included", False),
+        AlgorithmInfo("bdbsc", bdbs_excluded, "excluded", True),
+        AlgorithmInfo("box-complement", box_complement_excluded, "excluded", False),
+    )
+}
+
+
+def resolve_algorithm(name: str) -> AlgorithmInfo:
+    info = ALGORITHMS.get(name)
+    if info is None:
+        raise ConfigurationError(
+            f"unknown algorithm {name!r}; choose from {', '.join(sorted(ALGORITHMS))}"
+        )
+    return info
+
+
+def check_algorithm_config(info: AlgorithmInfo, ops, d=None) -> None:
+    """Reject impossible algorithm/monoid combinations before any work (bench.py:88-100)."""
+    _, _, has_inverse = device_operator(ops)
+    if info.needs_inverse and not has_inverse:
+        raise ConfigurationError(
+            f"algorithm {info.name!r} requires an invertible monoid, "
+            f"but {getattr(ops, 'name', ops)!r} has no inverse"
+        )
+    if d is not None and info.dims is not None and d not in info.dims:
+        raise ConfigurationError(f"algorithm {info.name!r} does not support {d}-D tensors")
+
+
+def register_with_reference(bench_module) -> None:
+    """Swap the reference's registry entries for the B200 routes.
+
+    ``bench_module`` is the reference's ``exsum.bench``; afterwards
+    ``exsum run --algo bdbs|bdbsc|box-complement`` executes on the GPU
+    (the monkeypatch precedent is test_bench.py:243-245).
+    """
+    ref_info = bench_module.AlgorithmInfo
+    for name, info in ALGORITHMS.items():
+        bench_module.ALGORITHMS[name] = ref_info(name, info.fn, info.kind, info.needs_inverse)

@@ -1,0 +1,72 @@
+"""Parity helpers shared by the GPU tests and bench.py (test infrastructure).
+
+Exactness contract (north star):
+  * int64 + and max: bit-exact, every route.
+  * float BDBS: bit-exact -- the kernels keep the reference's association
+    (in-block right-nested suffix, left-nested prefix, axes in order).
+  * float BDBSC and box-complement: |got - want| <= tau * S(x), where want is
+    the reference algorithm evaluated in float64 (the CPU oracle on the
+    float64-upcast input), S(x) is a magnitude bound of every partial sum that
+    feeds x, and tau = D * u with u the unit roundoff of the data type and D
+    a bound on the number of roundings on any path to x:
+      - BDBSC: S(x) = sum(|A|) (the total dominates), D = sum_i(2 k_i) + 8;
+      - box-complement: S(x) = box_complement(|A|)(x) + included(|A|)(x)
+        (all terms are partial sums of |A| over subsets of the array), and
+        D = sum_i(n_i + 2 k_i) + 16 (full-axis scans are the longest chains).
+    The float64 oracle's own error is D_ref * 2^-53 * S, negligible next to
+    float32's u = 2^-24; for float64 data both sides count.
+"""
+
+from __future__ import annotations
+
+import numpy as np
+
+U = {np.dtype(np.float32): 2.0**-24, np.dtype(np.float64): 2.0**-53}
+
+
+def depth(route, ext, k):
+    if route == "bdbs":
+        return sum(2 * kk for kk in k) + 4
+    if route == "bdbsc":
+        return sum(2 * kk for kk in k) + 8
+    return sum(n + 2 * kk for n, kk in zip(ext, k)) + 16
+
+
+def float_tolerance(route, a, k, oracle_mod):
+    """Elementwise tolerance array for a float route (see module docstring)."""
+    ext = a.shape
+    u = U[np.dtype(a.dtype)]
+    if np.dtype(a.dtype) == np.float64:
+        u = 2 * u  # both sides round in float64
+    a64 = np.abs(a.astype(np.float64))
+    D = depth(route, ext, k)
+    if route == "bdbsc":
+        S = np.full(ext, a64.sum())
+    elif route == "box-complement":
+        S = oracle_mod.box_complement_excluded(a64, k) + oracle_mod.bdbs_included(a64, k)
+    else:
+        S = oracle_mod.bdbs_included(a64, k)
+    return D * u * S + np.finfo(np.float64).tiny
+
+
+def compare(route, got, want, a, k, oracle_mod):
+    """Return (ok, max_err_over_tol, max_rel_err) per the exactness contract."""
+    got = np.asarray(got)
+    want = np.asarray(want)
+    if got.shape != want.shape:
+        return False, float("inf"), float("inf")
+    if got.dtype.kind != "f" or route == "bdbs":
+        ok = np.array_equal(got.view(np.uint8), want.astype(got.dtype).view(np.uint8))
+        return ok, 0.0 if ok else float("inf"), 0.0 if ok else float("inf")
+    tol = float_tolerance(route, a, k, oracle_mod)
+    err = np.abs(got.astype(np.float64) - want.astype(np.float64))
+    ratio = float(np.max(err / tol)) if err.size else 0.0
+    rel = float(np.max(err / np.maximum(np.abs(want.astype(np.float64)), 1e-300))) if err.size else 0.0
+    return ratio <= 1.0, ratio, rel
+
+
+def float64_oracle(route, a, box, oracle_mod, op="add"):
+    """Reference algorithm evaluated in float64 on the upcast input."""
+    if a.dtype.kind == "f":
+        return oracle_mod.ROUTES[route](a.astype(np.float64), box, op)
+    return oracle_mod.ROUTES[route](a, box, op)

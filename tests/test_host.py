@@ -1,0 +1,185 @@
+"""Host-side logic and the C-ABI boundary (CPU only; no kernel is executed)."""
+
+import ctypes
+import os
+import re
+
+import numpy as np
+import pytest
+
+import paper_2106_00124_b200 as ex
+from paper_2106_00124_b200 import _native
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+
+
+def _header_functions():
+    text = open(os.path.join(ROOT, "include", "exsum_b200.h")).read()
+    return re.findall(r"^\s*(?:const\s+)?\w+\s*\*?\s*(exsum_\w+)\s*\(", text, re.M)
+
+
+def test_library_exports_every_header_symbol():
+    L = _native.load()
+    names = _header_functions()
+    assert len(names) >= 10
+    for name in names:
+        assert hasattr(L, name), name
+    assert set(names) == set(_native.EXPORTS)
+    assert L.exsum_abi_version() == 1
+
+
+def test_library_is_sm100a():
+    blob = open(_native.LIB_PATH, "rb").read()
+    assert b"sm_100a" in blob
+
+
+def test_error_classes_mirror_reference():
+    assert issubclass(ex.UsageError, ValueError)
+    assert issubclass(ex.UsageError, ex.ExsumError)
+    assert issubclass(ex.ConfigurationError, ex.ExsumError)
+    assert issubclass(ex.VerificationError, ex.ExsumError)
+
+
+def test_normalize_box_like_reference():
+    assert ex.normalize_box((5, 5), (2, 9)) == (2, 5)
+    with pytest.raises(ex.UsageError):
+        ex.normalize_box((5, 5), (2,))
+    with pytest.raises(ex.UsageError):
+        ex.normalize_box((5, 5), (0, 1))
+    with pytest.raises(ex.UsageError):
+        ex.validate_extents((3, 0))
+    with pytest.raises(ex.UsageError):
+        ex.validate_extents(())
+
+
+def test_validation_happens_before_any_device_work():
+    t = ex.Tensor(ex.IntAddOps(), np.zeros((5, 5), dtype=np.int64))
+    with pytest.raises(ex.UsageError):
+        ex.bdbs_included(t, (2,))
+    with pytest.raises(ex.UsageError):
+        ex.box_complement_excluded(t, (2, 2, 2))
+    with pytest.raises(ex.UsageError):
+        ex.bdbs_excluded(t, (0, 1))
+    tm = ex.Tensor(ex.IntMaxOps(), np.zeros((5, 5), dtype=np.int64))
+    with pytest.raises(ex.ConfigurationError):
+        ex.bdbs_excluded(tm, (2, 2))
+    with pytest.raises(ex.ConfigurationError):
+        ex.resolve_monoid("mod-add:7")
+
+
+def test_unsupported_monoid_is_configuration_error():
+    class Weird:
+        name = "mod-add:11"
+        dtype = np.dtype(np.int64)
+        identity = 0
+
+    t = ex.Tensor(Weird(), np.zeros((3,), dtype=np.int64))
+    with pytest.raises(ex.ConfigurationError):
+        ex.bdbs_included(t, (2,))
+
+
+def test_reference_style_monoids_and_instrumentation_unwrap():
+    class RefAdd:  # duck-typed like exsum.IntAddOps
+        name = "add-i64"
+        dtype = np.dtype(np.int64)
+        identity = 0
+        has_inverse = True
+
+    class Instrumented:  # like exsum.InstrumentedMonoid (bench.py:128 unwraps .inner)
+        def __init__(self, inner):
+            self.inner = inner
+            self.name = inner.name
+            self.dtype = inner.dtype
+
+    from paper_2106_00124_b200.monoid import device_operator
+
+    assert device_operator(RefAdd()) == (np.dtype(np.int64), "add", True)
+    assert device_operator(Instrumented(RefAdd())) == (np.dtype(np.int64), "add", True)
+    assert device_operator(ex.IntMaxOps()) == (np.dtype(np.int64), "max", False)
+    assert device_operator(ex.Float32AddOps())[0] == np.dtype(np.float32)
+
+
+def test_no_cpu_fallback_without_gpu():
+    import torch
+
+    if torch.cuda.is_available():
+        pytest.skip("GPU present")
+    t = ex.Tensor(ex.IntAddOps(), np.arange(12, dtype=np.int64).reshape(3, 4))
+    with pytest.raises(ex.DeviceError):
+        ex.bdbs_included(t, (2, 2))
+
+
+def test_c_abi_validation_codes():
+    L = _native.load()
+    ext = _native.i64_array((4, 4))
+    box = _native.i64_array((2, 2))
+    out = ctypes.c_size_t(0)
+    assert L.exsum_workspace_bytes(0, 0, 0, 2, ext, box, ctypes.byref(out)) == 0
+    assert L.exsum_workspace_bytes(1, 2, 1, 2, ext, box, ctypes.byref(out)) == 2  # bdbsc + max
+    assert L.exsum_workspace_bytes(0, 1, 1, 2, ext, box, ctypes.byref(out)) == 2  # max-f64
+    assert L.exsum_workspace_bytes(0, 7, 0, 2, ext, box, ctypes.byref(out)) == 2  # dtype
+    assert L.exsum_workspace_bytes(0, 0, 0, 0, ext, box, ctypes.byref(out)) == 1  # d = 0
+    bad = _native.i64_array((0, 2))
+    assert L.exsum_workspace_bytes(0, 0, 0, 2, ext, bad, ctypes.byref(out)) == 1  # k = 0
+    assert b"box side" in L.exsum_last_error()
+    # device entry points refuse aliasing and null pointers before touching CUDA
+    assert L.exsum_bdbs_included(None, None, 0, 0, 2, ext, box, None, 0, None) == 1
+    assert L.exsum_bdbs_included(16, 16, 0, 0, 2, ext, box, None, 0, None) == 1
+
+
+def test_workspace_sizes():
+    # BDBS with >= 2 active passes needs one ping-pong array
+    n = 1 << 30
+    assert _native.workspace_bytes("bdbs", "float32", "add", (1024,) * 3, (16,) * 3) == 4 * n
+    assert _native.workspace_bytes("bdbs", "float32", "add", (1024, 1024), (1, 16)) == 0
+    # box-complement: W buffer + per-level reductions (<= N + small)
+    ws = _native.workspace_bytes("box-complement", "float32", "add", (1024,) * 3, (16,) * 3)
+    assert 4 * n <= ws <= 4 * n + 64 * 2**20
+
+
+def test_registry_mirrors_reference():
+    assert set(ex.ALGORITHMS) == {"bdbs", "bdbsc", "box-complement"}
+    info = ex.resolve_algorithm("bdbsc")
+    assert info.needs_inverse and info.kind == "excluded"
+    with pytest.raises(ex.ConfigurationError):
+        ex.check_algorithm_config(info, ex.IntMaxOps())
+    ex.check_algorithm_config(ex.resolve_algorithm("box-complement"), ex.IntMaxOps())
+    with pytest.raises(ex.ConfigurationError):
+        ex.resolve_algorithm("corners")
+
+
+def test_register_with_reference_registry():
+    from dataclasses import dataclass
+
+    @dataclass(frozen=True)
+    class AlgorithmInfo:
+        name: str
+        fn: object
+        kind: str
+        needs_inverse: bool
+        dims: object = None
+        cache_arg: str = ""
+
+    class FakeBench:
+        pass
+
+    fb = FakeBench()
+    fb.AlgorithmInfo = AlgorithmInfo
+    fb.ALGORITHMS = {"bdbs": None, "sat": "untouched"}
+    ex.register_with_reference(fb)
+    assert fb.ALGORITHMS["bdbs"].fn is ex.bdbs_included
+    assert fb.ALGORITHMS["box-complement"].fn is ex.box_complement_excluded
+    assert fb.ALGORITHMS["sat"] == "untouched"
+
+
+def test_pad_and_crop():
+    t = ex.Tensor(ex.IntAddOps(), np.arange(10, dtype=np.int64).reshape(2, 5))
+    p, ext = ex.pad_to_box_multiple(t, (2, 3))
+    assert p.extents == (2, 6) and ext == (2, 5)
+    assert p.data[0, 5] == 0
+    assert np.array_equal(ex.crop_to(p, ext).data, t.data)
+
+
+def test_tensor_dtype_check():
+    with pytest.raises(ex.UsageError):
+        ex.Tensor(ex.IntAddOps(), np.zeros(3, dtype=np.float64))

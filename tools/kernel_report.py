@@ -1,0 +1,106 @@
+"""Per-kernel device time and achieved HBM bandwidth for each config/route.
+
+    python tools/kernel_report.py [--configs c1,c2,c4,...] [--reps 3]
+
+Uses the library's CUDA-event profiler (exsum_profile_*): every launch is
+bracketed by events on its own stream; bytes are the kernel's algorithmic
+(compulsory) bytes.  Prints one JSON object per (config, route).
+"""
+
+import argparse
+import json
+import os
+import sys
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+sys.path.insert(0, ROOT)
+
+CASES = {
+    "c1": ((1024, 1024), "float64", [(32, 32)], ["bdbs"]),
+    "c2": ((256, 256, 256), "int64", [(8, 8, 8)], ["box-complement:max", "bdbsc", "bdbs:max"]),
+    "c3a": ((4096, 4096), "float32", [(4, 4)], ["bdbs", "bdbs-i64:max"]),
+    "c3b": ((256, 256, 256), "float32", [(4, 4, 4)], ["bdbs", "bdbs-i64:max"]),
+    "c3c": ((64, 64, 64, 64), "float32", [(4,) * 4], ["bdbs", "bdbs-i64:max"]),
+    "c3d": ((28,) * 5, "float32", [(4,) * 5], ["bdbs", "bdbs-i64:max"]),
+    "c3e": ((16,) * 6, "float32", [(4,) * 6], ["bdbs", "bdbs-i64:max"]),
+    "c4": ((1024, 1024, 1024), "float32", [(16, 16, 16)], ["box-complement", "bdbsc", "bdbs"]),
+    "c5": ((512, 512, 512), "float64", [(2, 2, 2), (8, 8, 8), (32, 32, 32), (128, 4, 1), (1, 1, 512)],
+           ["bdbs", "bdbsc"]),
+}
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--configs", default=",".join(CASES))
+    ap.add_argument("--reps", type=int, default=3)
+    args = ap.parse_args()
+    import torch
+
+    import paper_2106_00124_b200 as ex
+    from paper_2106_00124_b200 import _native
+
+    peak = json.load(open(os.path.join(ROOT, "MEASURED_PEAKS.json")))["hbm_gbs"] \
+        if os.path.exists(os.path.join(ROOT, "MEASURED_PEAKS.json")) else 6650.0
+    dev = torch.device("cuda:0")
+    for cname in args.configs.split(","):
+        ext, dtype, boxes, routes = CASES[cname]
+        g = torch.Generator(device=dev).manual_seed(0)
+        xf = torch.rand(ext, generator=g, device=dev,
+                        dtype=torch.float32 if dtype == "float32" else torch.float64) \
+            if dtype != "int64" else None
+        xi = None
+        for box in boxes:
+            for r in routes:
+                route, _, op = r.partition(":")
+                if route.endswith("-i64") or dtype == "int64":
+                    route = route.replace("-i64", "")
+                    if xi is None:
+                        xi = torch.randint(-2**20, 2**20, ext, generator=g, device=dev)
+                    x = xi
+                    ops = ex.IntMaxOps() if op == "max" else ex.IntAddOps()
+                else:
+                    x = xf
+                    ops = ex.Float32AddOps() if dtype == "float32" else ex.FloatAddOps()
+                fn = {"bdbs": ex.bdbs_included, "bdbsc": ex.bdbs_excluded,
+                      "box-complement": ex.box_complement_excluded}[route]
+                t = ex.Tensor(ops, x)
+                for _ in range(2):
+                    fn(t, box)
+                torch.cuda.synchronize()
+                _native.profile_enable(True)
+                a = torch.cuda.Event(enable_timing=True)
+                b = torch.cuda.Event(enable_timing=True)
+                a.record()
+                for _ in range(args.reps):
+                    o = fn(t, box)
+                    del o
+                b.record()
+                torch.cuda.synchronize()
+                recs = _native.profile_records()
+                _native.profile_enable(False)
+                step_ms = a.elapsed_time(b) / args.reps
+                per = {}
+                for name, by, ms in recs:
+                    key = f"{name}[{by / 1e6:.0f}MB]"
+                    d = per.setdefault(key, [0.0, 0.0, 0])
+                    d[0] += ms
+                    d[1] += by
+                    d[2] += 1
+                kern = {k: {"ms": v[0] / args.reps, "GBps": round(v[1] / v[0] / 1e6, 1),
+                            "frac": round(v[1] / v[0] / 1e6 / peak, 3)} for k, v in per.items()}
+                N = int(np.prod(ext))
+                es = x.element_size()
+                print(json.dumps({"config": cname, "route": route, "op": ops.name, "box": box,
+                                  "step_ms": round(step_ms, 4),
+                                  "Gelem_s": round(N / step_ms / 1e6, 2),
+                                  "compulsory_frac": round(2 * N * es / step_ms / 1e6 / peak, 3),
+                                  "kernels": kern}), flush=True)
+                del t
+        del xf, xi
+        torch.cuda.empty_cache()
+
+
+if __name__ == "__main__":
+    main()
