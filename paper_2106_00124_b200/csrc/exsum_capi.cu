@@ -155,44 +155,69 @@ PassPlan plan_passes(const Shape& s, int upto) {
   return p;
 }
 
-int run_passes(const Shape& s, const PassPlan& p, int dtype, int op, const void* src,
-               void* final_dst, void* other, const void* epi_total, cudaStream_t st,
-               int* launches) {
+// One windowed pass along axis a (profiled), optionally piggy-backing a
+// reduction over the raw input (PassExtra).
+int one_pass(const Shape& s, int a, int dtype, int op, const void* src, void* dst,
+             const void* epi_total, cudaStream_t st, int* launches, PassExtra* ex) {
+  const size_t es = dtype_size(dtype);
+  ProfScope ps(a == s.d - 1 ? "pass_rows" : "pass_strided", 2.0 * (double)s.N * es, st);
+  int rc = launch_pass(dtype, op, src, dst, prod(s.ext, 0, a), s.ext[a], prod(s.ext, a + 1, s.d),
+                       s.k[a], epi_total, st, ex);
+  if (rc < 0) return fail(EXSUM_ECONFIG, "no kernel for this dtype/operator");
+  *launches += rc;
+  return EXSUM_OK;
+}
+
+// Passes along p.axes, the first reading src, the last writing final_dst,
+// intermediates alternating with `other`.  after_first() runs (in both the
+// sizing and the launch pass) right after the first pass is enqueued.
+template <class F>
+int run_chain(const Shape& s, const PassPlan& p, int dtype, int op, const void* src,
+              void* final_dst, void* other, const void* epi_total, cudaStream_t st,
+              int* launches, bool live, PassExtra* ex0, F after_first) {
   const void* cur = src;
   for (int i = 0; i < p.count; ++i) {
-    const int a = p.axes[i];
     const int remaining = p.count - 1 - i;
     void* dst = (remaining % 2 == 0) ? final_dst : other;
-    const bool last = i == p.count - 1;
-    const size_t es = dtype_size(dtype);
-    ProfScope ps(a == s.d - 1 ? "pass_rows" : "pass_strided", 2.0 * (double)s.N * es, st);
-    int rc = launch_pass(dtype, op, cur, dst, prod(s.ext, 0, a), s.ext[a], prod(s.ext, a + 1, s.d),
-                         s.k[a], last ? epi_total : nullptr, st);
-    if (rc < 0) return fail(EXSUM_ECONFIG, "no kernel for this dtype/operator");
-    *launches += rc;
+    if (live) {
+      int rc = one_pass(s, p.axes[i], dtype, op, cur, dst, i == p.count - 1 ? epi_total : nullptr,
+                        st, launches, i == 0 ? ex0 : nullptr);
+      if (rc) return rc;
+    }
+    if (i == 0) {
+      int rc = after_first();
+      if (rc) return rc;
+    }
     cur = dst;
   }
   return EXSUM_OK;
 }
+
+int no_hook() { return EXSUM_OK; }
 
 // ------------------------------------------------------------------ routes --
 
 int route_bdbs(const Shape& s, int dtype, int op, const void* in, void* out, Arena& ar,
                bool complement, cudaStream_t st, int* launches) {
   const size_t es = dtype_size(dtype);
+  const bool live = ar.base != nullptr;
   PassPlan p = plan_passes(s, s.d);
+  void* partials = nullptr;
   void* total = nullptr;
   if (complement) {
-    void* partials = ar.take((size_t)reduce_partials_count() * 8);
+    partials = ar.take((size_t)reduce_partials_count() * 8);
     total = ar.take(8);
-    if (ar.base) {
+  }
+  void* other = p.count >= 2 ? ar.take((size_t)s.N * es) : nullptr;
+  auto full_total = [&]() {
+    if (live) {
       ProfScope ps("total", (double)s.N * es, st);
       *launches += launch_total(dtype, op, in, s.N, partials, total, st);
     }
-  }
-  void* other = p.count >= 2 ? ar.take((size_t)s.N * es) : nullptr;
-  if (!ar.base) return EXSUM_OK;
+  };
   if (p.count == 0) {
+    if (complement) full_total();
+    if (!live) return EXSUM_OK;
     ProfScope ps(complement ? "complement" : "copy", 2.0 * (double)s.N * es, st);
     if (complement) {
       *launches += launch_complement(dtype, in, out, s.N, total, st);
@@ -201,31 +226,77 @@ int route_bdbs(const Shape& s, int dtype, int op, const void* in, void* out, Are
     }
     return EXSUM_OK;
   }
-  return run_passes(s, p, dtype, op, in, out, other, total, st, launches);
+  const int d = s.d;
+  const bool fused = p.count >= 2 && p.axes[p.count - 2] == d - 2 && p.axes[p.count - 1] == d - 1 &&
+                     fused_pair_ok(dtype, op, s.ext[d - 1], s.k[d - 2], s.k[d - 1], ROW_WIN);
+  PassPlan head = p;
+  if (fused) head.count -= 2;
+  // BDBSC total: folded into the first pass when a later pass applies it
+  PassExtra ex0;
+  ex0.kind = 2;
+  ex0.buf = partials;
+  ex0.cap = reduce_partials_count();
+  const bool piggy = complement && head.count >= 1 && (fused || head.count >= 2);
+  if (complement && !piggy) full_total();
+  auto finish_total = [&]() -> int {
+    if (piggy && live) {
+      if (ex0.done) {
+        *launches += launch_total_final(dtype, op, partials, ex0.ppr, total, st);
+      } else {
+        full_total();
+      }
+    }
+    return EXSUM_OK;
+  };
+  const void* mid = in;
+  if (head.count > 0) {
+    void* head_dst = fused ? other : out;
+    void* head_other = fused ? out : other;
+    int rc = run_chain(s, head, dtype, op, in, head_dst, head_other, fused ? nullptr : total, st,
+                       launches, live, piggy ? &ex0 : nullptr, finish_total);
+    if (rc) return rc;
+    mid = head_dst;
+  }
+  if (fused && live) {
+    ProfScope ps("fused_pair", 2.0 * (double)s.N * es, st);
+    const int64_t n1 = s.ext[d - 2], n2 = s.ext[d - 1];
+    int rc = launch_fused_pair(dtype, op, mid, out, s.N / (n1 * n2), n1, n2, s.k[d - 2],
+                               s.k[d - 1], ROW_WIN, total, nullptr, st);
+    if (rc < 0) return fail(EXSUM_ECUDA, "fused pass pair failed to launch");
+    *launches += rc;
+  }
+  return EXSUM_OK;
 }
 
 // BC(src) -> dst, peeling the last axis (see file header).
 int route_box_complement(const Shape& s, int dtype, int op, const void* src, void* dst,
                          Arena& ar, cudaStream_t st, int* launches) {
   const size_t es = dtype_size(dtype);
+  const bool live = ar.base != nullptr;
   const int d = s.d;
   const int64_t n = s.ext[d - 1];
   const int64_t rows = s.N / n;
   if (d == 1) {
     void* scratch = ar.take(excl_rows_scratch_elems(dtype, 1, n) * es);
-    if (ar.base) {
+    if (live) {
       ProfScope ps("excl_rows", 2.0 * (double)n * es, st);
       *launches += launch_excl_rows(dtype, op, src, dst, nullptr, 1, n, s.k[0], scratch, st);
     }
     return EXSUM_OK;
   }
-  // R = reduction over the last axis; T = BC(R, k[:-1])
   void* R = ar.take((size_t)rows * es);
   void* T = ar.take((size_t)rows * es);
-  if (ar.base) {
-    ProfScope ps("row_reduce", (double)(s.N + rows) * es, st);
-    *launches += launch_row_reduce(dtype, op, src, R, rows, n, st);
-  }
+  PassPlan p = plan_passes(s, d - 1);  // W = windowed passes along axes 0..d-2
+  const bool fused = p.count > 0 && p.axes[p.count - 1] == d - 2 &&
+                     fused_pair_ok(dtype, op, n, s.k[d - 2], s.k[d - 1], ROW_EXCL);
+  PassPlan head = p;
+  if (fused) head.count -= 1;
+  // R = reduction over the last axis, folded into the first W pass when
+  // there is one (it reads the raw input anyway); then T = BC(R, k[:-1])
+  PassExtra ex0;
+  ex0.kind = 1;
+  ex0.row_len = n;
+  ex0.buf = head.count > 0 ? ar.take((size_t)(s.N / 32 + 1) * es) : nullptr;
   Shape t;
   t.d = d - 1;
   t.N = rows;
@@ -233,21 +304,43 @@ int route_box_complement(const Shape& s, int dtype, int op, const void* src, voi
     t.ext[i] = s.ext[i];
     t.k[i] = s.k[i];
   }
-  int rc = route_box_complement(t, dtype, op, R, T, ar, st, launches);
-  if (rc) return rc;
-  // W = windowed passes along axes 0..d-2 (never aliases dst)
-  PassPlan p = plan_passes(s, d - 1);
-  const void* W = src;
-  if (p.count > 0) {
-    void* wbuf = ar.take((size_t)s.N * es);
-    if (ar.base) {
-      rc = run_passes(s, p, dtype, op, src, wbuf, dst, nullptr, st, launches);
-      if (rc) return rc;
+  auto reduce_and_tail = [&]() -> int {
+    if (live) {
+      if (ex0.done) {
+        *launches += launch_rowpart_final(dtype, op, ex0.buf, R, rows, ex0.ppr, st);
+      } else {
+        ProfScope ps("row_reduce", (double)(s.N + rows) * es, st);
+        *launches += launch_row_reduce(dtype, op, src, R, rows, n, st);
+      }
     }
+    return route_box_complement(t, dtype, op, R, T, ar, st, launches);
+  };
+  const void* W = src;
+  if (head.count > 0) {
+    void* wbuf = ar.take((size_t)s.N * es);
+    // the chain ends in wbuf; dst serves as the ping-pong partner
+    int rc = run_chain(s, head, dtype, op, src, wbuf, dst, nullptr, st, launches, live, &ex0,
+                       reduce_and_tail);
+    if (rc) return rc;
     W = wbuf;
+  } else {
+    int rc = reduce_and_tail();
+    if (rc) return rc;
+  }
+  if (fused) {
+    // last W pass (axis d-2) fused with the row round (fused_pair.cu)
+    if (live) {
+      ProfScope ps("fused_pair", (double)(2 * s.N + rows) * es, st);
+      const int64_t n1 = s.ext[d - 2];
+      int rc = launch_fused_pair(dtype, op, W, dst, s.N / (n1 * n), n1, n, s.k[d - 2], s.k[d - 1],
+                                 ROW_EXCL, nullptr, T, st);
+      if (rc < 0) return fail(EXSUM_ECUDA, "fused pass pair failed to launch");
+      *launches += rc;
+    }
+    return EXSUM_OK;
   }
   void* scratch = ar.take(excl_rows_scratch_elems(dtype, rows, n) * es);
-  if (ar.base) {
+  if (live) {
     ProfScope ps("excl_rows", (double)(2 * s.N + rows) * es, st);
     *launches += launch_excl_rows(dtype, op, W, dst, T, rows, n, s.k[d - 1], scratch, st);
   }

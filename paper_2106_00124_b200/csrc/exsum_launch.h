@@ -20,8 +20,28 @@ enum OpCode { ADD = 0, MAX = 1 };
 // stitch combine).  in != out.  `total` (device, nullable) turns on the BDBSC
 // complement epilogue out = total (-) value (float32 data: total is a double).
 // Returns the number of kernels launched.
+// Optional work piggy-backed on a strided pass over the raw input:
+//   kind 1: per-warp row partials of the last axis (row_len elements per row)
+//           into buf; on success ppr = partials per row (finish with
+//           launch_rowpart_final);
+//   kind 2: per-CTA partial totals into buf (capacity cap); on success ppr =
+//           number of partials (finish with launch_total_final).
+struct PassExtra {
+  int kind = 0;
+  void* buf = nullptr;
+  int64_t row_len = 0;
+  int64_t cap = 0;
+  int done = 0;
+  int64_t ppr = 0;
+};
+
 int launch_pass(int dtype, int op, const void* in, void* out, int64_t outer, int64_t n,
-                int64_t inner, int64_t k, const void* total, cudaStream_t s);
+                int64_t inner, int64_t k, const void* total, cudaStream_t s,
+                PassExtra* ex = nullptr);
+int launch_rowpart_final(int dtype, int op, const void* part, void* R, int64_t rows, int64_t ppr,
+                         cudaStream_t s);
+int launch_total_final(int dtype, int op, const void* partials, int64_t np, void* total,
+                       cudaStream_t s);
 
 // Deterministic total fold of N elements into *total (device; double for
 // float32).  partials: device scratch of reduce_partials_count() accumulators.
@@ -46,6 +66,16 @@ int launch_row_reduce(int dtype, int op, const void* in, void* R, int64_t rows, 
 int launch_excl_rows(int dtype, int op, const void* W, void* out, const void* T, int64_t rows,
                      int64_t n, int64_t k, void* scratch, cudaStream_t s);
 size_t excl_rows_scratch_elems(int dtype, int64_t rows, int64_t n);
+
+// Fused pass pair over [outer, n1, n2]: the windowed pass along n1 (window
+// k1) followed by a row op along n2 -- ROW_WIN: windowed pass with window k2
+// (+ BDBSC epilogue when total != nullptr); ROW_EXCL: box-complement round with
+// shift k2 and tail T (nullable).  fused_pair_ok() decides eligibility.
+enum { ROW_WIN = 0, ROW_EXCL = 1 };
+int fused_pair_ok(int dtype, int op, int64_t n2, int64_t k1, int64_t k2, int mode);
+int launch_fused_pair(int dtype, int op, const void* in, void* out, int64_t outer, int64_t n1,
+                      int64_t n2, int64_t k1, int64_t k2, int mode, const void* total,
+                      const void* Tail, cudaStream_t s);
 
 size_t dtype_size(int dtype);
 int num_sms();

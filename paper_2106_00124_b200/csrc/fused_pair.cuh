@@ -1,0 +1,384 @@
+// fused_pair.cuh -- the last two axes in one pass over HBM.
+//
+// Fuses the windowed pass along axis d-2 (scan.py:61-102, strided) with the
+// row operation along the contiguous axis d-1:
+//   ROW_WIN  : the windowed pass along axis d-1 (bdbs_included's last two
+//              passes, included.py:127-128; with the BDBSC complement epilogue,
+//              excluded.py:72-75)
+//   ROW_EXCL : the box-complement round of the peeled last axis,
+//              out = P[x-1] (+) S[x+k] (+) T[row] (excluded.py:151-156 restated;
+//              see exsum_capi.cu)
+// so the intermediate array never goes back to HBM: 2*N*s bytes instead of 4.
+//
+// B200 mapping: one CTA owns a slab [x1-segment, full rows] of one outer index
+// and streams it in blocks of k1 rows:
+//   * every thread owns one 16-byte column vector of the row and prefetches
+//     its own vectors of blocks b+2, b+3 with cp.async (LDGSTS) into a 2-slot
+//     shared ring -- no CTA barrier is needed for the loads, and two blocks of
+//     loads (128 KB at the C4 shape) are in flight while block b is processed;
+//   * the axis-(d-2) pass runs in registers exactly as in pass_strided.cu
+//     (suffix of block b, running prefix of block b+1), writing the k1 output
+//     rows to a padded shared stage (chunk stride an odd number of 16-byte
+//     vectors: conflict-free for both access patterns);
+//   * after one __syncthreads each warp takes whole rows, each lane a chunk of
+//     C = n2/32 consecutive elements in registers, and runs the row op
+//     (sequential exact in-block scans for ROW_WIN; lane fold + warp scans for
+//     ROW_EXCL), writing back in place; after a second __syncthreads the rows
+//     leave as coalesced 16-byte stores.
+// Float association: ROW_WIN keeps the reference's nesting, so BDBS stays
+// bit-exact; ROW_EXCL is reassociated (tolerance).
+#pragma once
+
+#include <stdlib.h>
+
+#include "exsum_common.cuh"
+#include "exsum_launch.h"
+
+namespace exsum {
+
+// K1: window along axis d-2 (compile time); the ROW_WIN row op uses the same
+// window along the row (K2 == K1, the cubic boxes of the BASELINE configs);
+// ROW_EXCL takes any shift kx at run time.
+template <class T, class Op, int C, int K1, int MODE>
+__global__ void __launch_bounds__(32 * C / (16 / sizeof(T)), 1)
+k_fused_pair(const T* __restrict__ in, T* __restrict__ out, int64_t outer, int64_t n1,
+             int64_t kx, int64_t seg_len, int64_t nseg,
+             const typename AccOf<T>::type* __restrict__ total, const T* __restrict__ Tail) {
+  constexpr int VE = 16 / sizeof(T);
+  constexpr int N2 = 32 * C;           // row length
+  constexpr int NT = N2 / VE;          // threads: one 16-byte column vector each
+  constexpr int NW = NT / 32;
+  constexpr int CV = C / VE;           // vectors per lane chunk
+  constexpr int PSV = (CV + 1) | 1;    // padded chunk stride in vectors (odd)
+  constexpr int CH = PSV * VE;         // padded chunk stride (elements)
+  constexpr int ROWP = 32 * CH;        // padded row length (elements)
+  constexpr int K2 = K1;
+  constexpr int M2 = C / K2;           // row-op blocks per lane chunk
+  constexpr int G = 16 / K1 > 0 ? 16 / K1 : 1;  // blocks per unit
+  constexpr int U = G * K1;            // rows per unit: register tile, stage, prefetch granule
+  static_assert(C % VE == 0 && (MODE == ROW_EXCL || C % K2 == 0), "shape");
+  typedef Vec<T, VE> VT;
+  extern __shared__ __align__(16) unsigned char smem[];
+  T* raw = reinterpret_cast<T*>(smem);  // [2][U][N2]
+  T* wst = raw + 2 * U * N2;            // [U][ROWP]
+  const int tid = threadIdx.x;
+  const int lane = tid & 31;
+  const int warp = tid >> 5;
+  const int col = tid * VE;
+  const int pcol = (col / C) * CH + (col % C);
+  const T ident = Op::template identity<T>();
+  const T tot = total ? (T)(*total) : T(0);
+  const bool epi = total != nullptr;
+  const int64_t last_bs = (int64_t)K1 * ((n1 - 1) / K1);
+  const int64_t items = outer * nseg;
+  const bool kvec = (kx % VE) == 0;
+
+  for (int64_t item = blockIdx.x; item < items; item += gridDim.x) {
+    const int64_t o = item / nseg;
+    const int64_t seg = item % nseg;
+    const int64_t xs = seg * seg_len;  // multiple of U
+    const int64_t xe = xs + seg_len < n1 ? xs + seg_len : n1;
+    const int64_t u0 = xs / U;
+    const int64_t u_end = (xe + U - 1) / U;
+    const T* src = in + o * n1 * N2 + col;
+    T* dst = out + o * n1 * N2 + col;
+
+    // rows loaded for unit ui: the whole unit inside the segment; past the
+    // segment only the first block's K1-1 rows (the stitch partner)
+    auto rows_of = [&](int64_t ui) -> int {
+      const int64_t avail = n1 - ui * U;
+      const int64_t want = ui >= u_end ? K1 - 1 : U;
+      return (int)(avail < want ? (avail > 0 ? avail : 0) : want);
+    };
+    auto issue = [&](int64_t ui) {
+      const int rows = rows_of(ui);
+      T* d = raw + ((ui - u0) & 1) * (U * N2) + col;
+      for (int r = 0; r < rows; ++r) cp_async16(d + r * N2, src + (ui * U + r) * N2);
+      cp_async_commit();  // always commit: uniform group accounting
+    };
+
+    issue(u0);
+    issue(u0 + 1);
+    cp_async_wait<1>();
+    VT cur[U];  // raw rows of the current unit
+    int len = rows_of(u0);
+#pragma unroll
+    for (int r = 0; r < U; ++r)
+      if (r < len) cur[r] = *reinterpret_cast<const VT*>(raw + col + r * N2);
+    issue(u0 + 2);
+
+    for (int64_t u = u0; u < u_end; ++u) {
+      const int64_t us = u * U;
+      const int rows_u = len;
+      if (us + rows_u < n1) cp_async_wait<1>();  // unit u+1 (its first block) has landed
+      const T* sn = raw + ((u + 1 - u0) & 1) * (U * N2) + col;
+#pragma unroll
+      for (int jb = 0; jb < G; ++jb) {
+        const int64_t bs = us + (int64_t)jb * K1;
+        if (jb * K1 < rows_u) {
+          const int blen = (int)(n1 - bs < K1 ? n1 - bs : K1);
+          // in-block suffix S (right nested), in place
+#pragma unroll
+          for (int r = K1 - 2; r >= 0; --r)
+            if (r < blen - 1) {
+#pragma unroll
+              for (int j = 0; j < VE; ++j)
+                cur[jb * K1 + r].v[j] = Op::apply(cur[jb * K1 + r].v[j], cur[jb * K1 + r + 1].v[j]);
+            }
+          if (bs == last_bs) {  // last block of axis d-2: W = S
+#pragma unroll
+            for (int r = 0; r < K1; ++r)
+              if (r < blen) *reinterpret_cast<VT*>(wst + (jb * K1 + r) * ROWP + pcol) = cur[jb * K1 + r];
+          } else {
+            // stitch with the next block's left-nested prefix (raw)
+            const int64_t nrows = n1 - bs - K1;
+            const int nlen = (int)(nrows < K1 ? nrows : K1);
+            *reinterpret_cast<VT*>(wst + (jb * K1) * ROWP + pcol) = cur[jb * K1];
+            const int nb0 = jb + 1 < G ? (jb + 1) * K1 : 0;  // in range for the dead branch
+            VT P;
+            if (jb + 1 < G) {
+              P = cur[nb0];
+            } else {
+              P = *reinterpret_cast<const VT*>(sn);
+            }
+#pragma unroll
+            for (int r = 1; r < K1; ++r) {
+              const int jj = r - 1;
+              if (jj >= 1 && jj < nlen) {
+                VT a;
+                if (jb + 1 < G) {
+                  a = cur[nb0 + jj];
+                } else {
+                  a = *reinterpret_cast<const VT*>(sn + jj * N2);
+                }
+#pragma unroll
+                for (int j = 0; j < VE; ++j) P.v[j] = Op::apply(P.v[j], a.v[j]);
+              }
+              VT w;
+#pragma unroll
+              for (int j = 0; j < VE; ++j) w.v[j] = Op::apply(cur[jb * K1 + r].v[j], P.v[j]);
+              *reinterpret_cast<VT*>(wst + (jb * K1 + r) * ROWP + pcol) = w;
+            }
+          }
+        }
+      }
+      // next unit's raw rows into registers; its slot is then free to refill
+      len = rows_of(u + 1);
+      if (u + 1 < u_end) {
+#pragma unroll
+        for (int r = 0; r < U; ++r)
+          if (r < len) cur[r] = *reinterpret_cast<const VT*>(sn + r * N2);
+      }
+      issue(u + 3);
+      __syncthreads();
+
+      // ---- row operation on the rows_u rows of the stage (warp per row) ----
+      for (int rr = warp; rr < rows_u; rr += NW) {
+        T* wrow = wst + rr * ROWP;
+        T* mine = wrow + lane * CH;
+        T a[C];
+#pragma unroll
+        for (int v = 0; v < CV; ++v) {
+          const VT q = *reinterpret_cast<const VT*>(mine + v * VE);
+#pragma unroll
+          for (int j = 0; j < VE; ++j) a[v * VE + j] = q.v[j];
+        }
+        if constexpr (MODE == ROW_WIN) {
+          // exact in-block scans along the row (blocks of K2 inside the chunk)
+          constexpr int NBV = (K2 + VE - 1) / VE;
+          VT nbv[NBV];  // neighbour's first block, raw
+          if (lane < 31) {
+#pragma unroll
+            for (int v = 0; v < NBV; ++v)
+              nbv[v] = *reinterpret_cast<const VT*>(wrow + (lane + 1) * CH + v * VE);
+          }
+#pragma unroll
+          for (int j = 0; j < M2; ++j) {
+#pragma unroll
+            for (int r = K2 - 2; r >= 0; --r) a[j * K2 + r] = Op::apply(a[j * K2 + r], a[j * K2 + r + 1]);
+            const bool last = (lane == 31) && (j == M2 - 1);  // n2 % K2 == 0
+            if (!last) {
+              if (j + 1 < M2) {
+                T Pr = a[(j + 1) * K2];
+#pragma unroll
+                for (int r = 1; r < K2; ++r) {
+                  if (r >= 2) Pr = Op::apply(Pr, a[(j + 1) * K2 + r - 1]);
+                  a[j * K2 + r] = Op::apply(a[j * K2 + r], Pr);
+                }
+              } else {
+                T Pr = nbv[0].v[0];
+#pragma unroll
+                for (int r = 1; r < K2; ++r) {
+                  if (r >= 2) Pr = Op::apply(Pr, nbv[(r - 1) / VE].v[(r - 1) % VE]);
+                  a[j * K2 + r] = Op::apply(a[j * K2 + r], Pr);
+                }
+              }
+            }
+          }
+          __syncwarp();
+#pragma unroll
+          for (int v = 0; v < CV; ++v) {
+            VT q;
+#pragma unroll
+            for (int j = 0; j < VE; ++j) {
+              const T w = a[v * VE + j];
+              q.v[j] = epi ? OpAdd::inverse<T>(tot, w) : w;
+            }
+            *reinterpret_cast<VT*>(mine + v * VE) = q;
+          }
+        } else {
+          // full-row prefix / suffix: lane fold, warp scans, S in place
+          T lt = a[0];
+#pragma unroll
+          for (int j = 1; j < C; ++j) lt = Op::apply(lt, a[j]);
+          T pin = lt, sin = lt;
+#pragma unroll
+          for (int d = 1; d < 32; d <<= 1) {
+            const T tp = __shfl_up_sync(0xffffffffu, pin, d);
+            const T ts = __shfl_down_sync(0xffffffffu, sin, d);
+            if (lane >= d) pin = Op::apply(tp, pin);
+            if (lane + d < 32) sin = Op::apply(sin, ts);
+          }
+          T pre = __shfl_up_sync(0xffffffffu, pin, 1);
+          T suf = __shfl_down_sync(0xffffffffu, sin, 1);
+          if (lane == 0) pre = ident;
+          if (lane == 31) suf = ident;
+          {
+            T run = suf;
+#pragma unroll
+            for (int v = CV - 1; v >= 0; --v) {
+              VT q;
+#pragma unroll
+              for (int j = VE - 1; j >= 0; --j) {
+                run = Op::apply(a[v * VE + j], run);
+                q.v[j] = run;
+              }
+              *reinterpret_cast<VT*>(mine + v * VE) = q;
+            }
+          }
+          __syncwarp();
+          const T tail = Tail ? Tail[o * n1 + us + rr] : ident;
+          T pe = pre;
+          if (kvec) {
+            // the shift keeps vector alignment: S[x+k] read as 16-byte vectors
+#pragma unroll
+            for (int v = 0; v < CV; ++v) {
+              const int64_t y0 = (int64_t)lane * C + v * VE + kx;
+              VT sq;
+              if (y0 < N2) {
+                sq = *reinterpret_cast<const VT*>(wrow + (y0 / C) * CH + (y0 % C));
+              } else {
+#pragma unroll
+                for (int j = 0; j < VE; ++j) sq.v[j] = ident;
+              }
+#pragma unroll
+              for (int j = 0; j < VE; ++j) {
+                const T ov = Op::apply(Op::apply(pe, sq.v[j]), tail);
+                pe = Op::apply(pe, a[v * VE + j]);
+                a[v * VE + j] = ov;
+              }
+            }
+          } else {
+#pragma unroll
+            for (int j = 0; j < C; ++j) {
+              const int64_t y = (int64_t)lane * C + j + kx;
+              const T sv = y < N2 ? wrow[(y / C) * CH + (y % C)] : ident;
+              const T ov = Op::apply(Op::apply(pe, sv), tail);
+              pe = Op::apply(pe, a[j]);
+              a[j] = ov;
+            }
+          }
+          __syncwarp();
+#pragma unroll
+          for (int v = 0; v < CV; ++v) {
+            VT q;
+#pragma unroll
+            for (int j = 0; j < VE; ++j) q.v[j] = a[v * VE + j];
+            *reinterpret_cast<VT*>(mine + v * VE) = q;
+          }
+        }
+        __syncwarp();
+      }
+      __syncthreads();
+      for (int r = 0; r < rows_u; ++r)
+        st_stream<T, VE>(dst + (us + r) * N2, *reinterpret_cast<const VT*>(wst + r * ROWP + pcol));
+    }
+    cp_async_wait<0>();
+  }
+}
+
+template <class T, class Op, int C, int K1, int MODE>
+int go_pair(const T* in, T* out, int64_t outer, int64_t n1, int64_t kx,
+            const typename AccOf<T>::type* total, const T* Tail, cudaStream_t s) {
+  constexpr int VE = 16 / sizeof(T);
+  constexpr int N2 = 32 * C;
+  constexpr int NT = N2 / VE;
+  constexpr int CV = C / VE;
+  constexpr int PSV = (CV + 1) | 1;
+  constexpr int ROWP = 32 * PSV * VE;
+  constexpr int U = (16 / K1) * K1;
+  const size_t smem = ((size_t)2 * U * N2 + (size_t)U * ROWP) * sizeof(T);
+  if (smem > 220 * 1024) return -1;
+  int per_sm = (int)((228 * 1024) / (smem + 1024));
+  if (per_sm > 2048 / NT) per_sm = 2048 / NT;
+  if (per_sm < 1) per_sm = 1;
+  const int64_t nunits = (n1 + U - 1) / U;
+  // enough CTAs for ~3 waves of resident CTAs; segments keep >= 4 units
+  const int64_t want = (int64_t)num_sms() * per_sm * 3;
+  int64_t nseg = (want + outer - 1) / outer;
+  int64_t max_seg = nunits / 4;
+  if (max_seg < 1) max_seg = 1;
+  if (nseg > max_seg) nseg = max_seg;
+  if (nseg < 1) nseg = 1;
+  const int64_t seg_len = U * ((nunits + nseg - 1) / nseg);
+  nseg = (n1 + seg_len - 1) / seg_len;
+  const int64_t items = outer * nseg;
+  int64_t grid = items;
+  const int64_t cap = (int64_t)num_sms() * per_sm * 4;
+  if (grid > cap) grid = cap;
+  cudaFuncSetAttribute(k_fused_pair<T, Op, C, K1, MODE>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                       (int)smem);
+  k_fused_pair<T, Op, C, K1, MODE><<<(unsigned)grid, NT, smem, s>>>(in, out, outer, n1, kx, seg_len,
+                                                                   nseg, total, Tail);
+  return 1;
+}
+
+template <class T, class Op, int C, int MODE>
+int pick_k1(const T* in, T* out, int64_t outer, int64_t n1, int64_t k1, int64_t kx,
+            const typename AccOf<T>::type* total, const T* Tail, cudaStream_t s) {
+  switch (k1) {
+    case 2: return go_pair<T, Op, C, 2, MODE>(in, out, outer, n1, kx, total, Tail, s);
+    case 4: return go_pair<T, Op, C, 4, MODE>(in, out, outer, n1, kx, total, Tail, s);
+    case 8: return go_pair<T, Op, C, 8, MODE>(in, out, outer, n1, kx, total, Tail, s);
+    case 16:
+      if constexpr (C >= 16) return go_pair<T, Op, C, 16, MODE>(in, out, outer, n1, kx, total, Tail, s);
+      return -1;
+  }
+  return -1;
+}
+
+template <class T, class Op>
+int go_fused(const T* in, T* out, int64_t outer, int64_t n1, int64_t n2, int64_t k1, int64_t k2,
+             int mode, const typename AccOf<T>::type* total, const T* Tail, cudaStream_t s) {
+  if (((uintptr_t)in % 16) || ((uintptr_t)out % 16)) return -1;
+  if (mode == ROW_WIN) {
+    switch (n2) {
+      case 256: return pick_k1<T, Op, 8, ROW_WIN>(in, out, outer, n1, k1, 0, total, nullptr, s);
+      case 512: return pick_k1<T, Op, 16, ROW_WIN>(in, out, outer, n1, k1, 0, total, nullptr, s);
+      case 1024:
+        if constexpr (sizeof(T) == 4) return pick_k1<T, Op, 32, ROW_WIN>(in, out, outer, n1, k1, 0, total, nullptr, s);
+        return -1;
+    }
+  } else {
+    switch (n2) {
+      case 256: return pick_k1<T, Op, 8, ROW_EXCL>(in, out, outer, n1, k1, k2, nullptr, Tail, s);
+      case 512: return pick_k1<T, Op, 16, ROW_EXCL>(in, out, outer, n1, k1, k2, nullptr, Tail, s);
+      case 1024:
+        if constexpr (sizeof(T) == 4) return pick_k1<T, Op, 32, ROW_EXCL>(in, out, outer, n1, k1, k2, nullptr, Tail, s);
+        return -1;
+    }
+  }
+  return -1;
+}
+
+}  // namespace exsum

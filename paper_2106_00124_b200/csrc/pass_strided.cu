@@ -20,18 +20,80 @@
 // k > 32 uses k_strided_blocks: one thread per (column-vector, block) and
 // two sweeps; the suffix sweep's results round-trip through the output buffer
 // (L2-resident at that distance) so no per-thread block storage is needed.
+#include <stdlib.h>
+#include <string.h>
+
 #include "exsum_common.cuh"
 #include "exsum_launch.h"
 #include "generic_blocks.cuh"
 
 namespace exsum {
 
-template <class T, class Op, int KMAX, int V>
+static int strided_mode();
+
+// EXTRA: 0 plain; 1 also folds every raw row segment of 32*V elements into
+// rowpart (the box-complement reduction R over the last axis, finished by
+// k_rowpart_final); 2 also folds all raw values into one partial per CTA
+// (the BDBSC total, finished by k_total_final).  Both reuse loads the pass
+// makes anyway, saving a full read of the array.
+template <class T, class Op, int KMAX, int V, int EXTRA = 0>
 __global__ void __launch_bounds__(256)
 k_strided_reg(const T* __restrict__ in, T* __restrict__ out, int64_t outer, int64_t n,
               int64_t inner, int k, int64_t seg_len, int64_t nseg,
-              const typename AccOf<T>::type* __restrict__ total) {
+              const typename AccOf<T>::type* __restrict__ total, T* __restrict__ rowpart = nullptr,
+              int64_t row_len = 0, typename AccOf<T>::type* __restrict__ tpart = nullptr) {
   typedef Vec<T, V> VT;
+  typedef typename AccOf<T>::type Acc;
+  Acc tacc[V];
+#pragma unroll
+  for (int j = 0; j < V; ++j) tacc[j] = Op::template identity<Acc>();
+  const int lane = threadIdx.x & 31;
+  // EXTRA == 1: fold the KMAX rows of a freshly loaded block across the warp's
+  // 32 lanes with a multi-value butterfly (KMAX-1 + 5-log2(KMAX) shuffles for
+  // KMAX rows, instead of 5 per row); lanes whose low bits are zero end up
+  // holding one row's sum each and store it to rowpart[part][row].
+  auto extra_block = [&](const VT (&blk)[KMAX], int nrows, int64_t o, int64_t x0, int64_t c) {
+    if constexpr (EXTRA == 1) {
+      T sv[KMAX];
+#pragma unroll
+      for (int r = 0; r < KMAX; ++r) {
+        T sum = blk[r].v[0];
+#pragma unroll
+        for (int j = 1; j < V; ++j) sum = Op::apply(sum, blk[r].v[j]);
+        sv[r] = r < nrows ? sum : Op::template identity<T>();
+      }
+      int rowbase = 0;
+#pragma unroll
+      for (int cnt = KMAX, off = 16; cnt > 1; cnt >>= 1, off >>= 1) {
+        const int half = cnt >> 1;
+        const bool hi = (lane & off) != 0;
+#pragma unroll
+        for (int i = 0; i < half; ++i) {
+          const T send = hi ? sv[i] : sv[i + half];
+          const T keep = hi ? sv[i + half] : sv[i];
+          sv[i] = Op::apply(keep, __shfl_xor_sync(0xffffffffu, send, off));
+        }
+        rowbase += hi ? half : 0;
+      }
+      constexpr int LOWB = 32 / KMAX;  // lanes still sharing a row
+#pragma unroll
+      for (int off = LOWB >> 1; off >= 1; off >>= 1)
+        sv[0] = Op::apply(sv[0], __shfl_xor_sync(0xffffffffu, sv[0], off));
+      if ((lane & (LOWB - 1)) == 0 && rowbase < nrows) {
+        const int64_t c0 = c - lane;  // the warp's first column vector
+        const int64_t e = (o * n + x0 + rowbase) * inner + c0 * V;
+        const int64_t rows_total = outer * n * inner / row_len;
+        rowpart[((e % row_len) / (32 * V)) * rows_total + e / row_len] = sv[0];
+      }
+    } else if constexpr (EXTRA == 2) {
+#pragma unroll
+      for (int r = 0; r < KMAX; ++r)
+        if (r < nrows) {
+#pragma unroll
+          for (int j = 0; j < V; ++j) tacc[j] = Op::apply(tacc[j], (Acc)blk[r].v[j]);
+        }
+    }
+  };
   const int64_t cv = inner / V;  // column vectors per outer slab
   const int64_t items = outer * cv * nseg;
   const T tot = total ? (T)(*total) : T(0);
@@ -55,6 +117,10 @@ k_strided_reg(const T* __restrict__ in, T* __restrict__ out, int64_t outer, int6
 #pragma unroll
     for (int r = 0; r < KMAX; ++r)
       if (r < len) cur[r] = ld_stream<T, V>(pin + (bs + r) * inner);
+    if constexpr (EXTRA != 0) {
+      const int64_t inseg = xe - bs;
+      extra_block(cur, (int)(len < inseg ? len : inseg), o, bs, c);
+    }
     // in-block suffix, right nested: S[r] = a[r] (+) S[r+1]   (scan.py:75-79)
 #pragma unroll
     for (int r = KMAX - 2; r >= 0; --r)
@@ -87,6 +153,10 @@ k_strided_reg(const T* __restrict__ in, T* __restrict__ out, int64_t outer, int6
 #pragma unroll
       for (int r = 0; r < KMAX; ++r)
         if (r < nlen) nxt[r] = ld_stream<T, V>(pin + (ns + r) * inner);
+      if constexpr (EXTRA != 0) {
+        const int64_t inseg = xe - ns;  // rows of this block inside the segment
+        extra_block(nxt, more ? (int)(nlen < inseg ? nlen : inseg) : 0, o, ns, c);
+      }
 
       // stitch (scan.py:88-102): out[bs] = S[bs]; out[bs+r] = S (+) P[min(r-1, nlen-1)]
       {
@@ -126,6 +196,21 @@ k_strided_reg(const T* __restrict__ in, T* __restrict__ out, int64_t outer, int6
         }
 #pragma unroll
       for (int r = 0; r < KMAX; ++r) cur[r] = nxt[r];
+    }
+  }
+  if constexpr (EXTRA == 2) {
+    __shared__ Acc sh[8];
+    Acc ta = tacc[0];
+#pragma unroll
+    for (int j = 1; j < V; ++j) ta = Op::apply(ta, tacc[j]);
+#pragma unroll
+    for (int d = 16; d >= 1; d >>= 1) ta = Op::apply(ta, __shfl_xor_sync(0xffffffffu, ta, d));
+    if (lane == 0) sh[threadIdx.x >> 5] = ta;
+    __syncthreads();
+    if (threadIdx.x == 0) {
+      Acc t = sh[0];
+      for (int w = 1; w < (int)(blockDim.x >> 5); ++w) t = Op::apply(t, sh[w]);
+      tpart[blockIdx.x] = t;
     }
   }
 }
@@ -223,7 +308,7 @@ int g_num_sms = 0;
 
 template <class T, class Op, int KMAX, int V>
 int go_reg(const T* in, T* out, int64_t outer, int64_t n, int64_t inner, int k,
-           const typename AccOf<T>::type* total, cudaStream_t s) {
+           const typename AccOf<T>::type* total, cudaStream_t s, PassExtra* ex) {
   const int64_t lines = outer * (inner / V);
   // split the axis into k-aligned segments until ~2 waves of 256-thread
   // blocks are resident; keep segments >= 16 blocks so the halo stays small
@@ -244,6 +329,21 @@ int go_reg(const T* in, T* out, int64_t outer, int64_t n, int64_t inner, int k,
   int64_t grid = (items + 255) / 256;
   const int64_t cap = (int64_t)num_sms() * 64;
   if (grid > cap) grid = cap;
+  typedef typename AccOf<T>::type Acc;
+  if (ex && ex->kind == 1 && ex->row_len % (32 * V) == 0 && (inner / V) % 32 == 0) {
+    k_strided_reg<T, Op, KMAX, V, 1><<<(unsigned)grid, 256, 0, s>>>(
+        in, out, outer, n, inner, k, seg_len, nseg, total, (T*)ex->buf, ex->row_len, nullptr);
+    ex->done = 1;
+    ex->ppr = ex->row_len / (32 * V);
+    return 1;
+  }
+  if (ex && ex->kind == 2 && grid <= ex->cap) {
+    k_strided_reg<T, Op, KMAX, V, 2><<<(unsigned)grid, 256, 0, s>>>(
+        in, out, outer, n, inner, k, seg_len, nseg, total, nullptr, 0, (Acc*)ex->buf);
+    ex->done = 1;
+    ex->ppr = grid;
+    return 1;
+  }
   k_strided_reg<T, Op, KMAX, V><<<(unsigned)grid, 256, 0, s>>>(in, out, outer, n, inner, k,
                                                                seg_len, nseg, total);
   return 1;
@@ -251,29 +351,40 @@ int go_reg(const T* in, T* out, int64_t outer, int64_t n, int64_t inner, int k,
 
 template <class T, class Op, int V>
 int go_v(const T* in, T* out, int64_t outer, int64_t n, int64_t inner, int64_t k,
-         const typename AccOf<T>::type* total, cudaStream_t s) {
+         const typename AccOf<T>::type* total, cudaStream_t s, PassExtra* ex) {
   // register tile 2*KMAX vectors of V elements: keep KMAX*WORDS <= 64
   // (128 data registers per thread; beyond that ptxas spills)
   constexpr int WORDS = (int)(sizeof(T) * V / 4);
-  if (k <= 2) return go_reg<T, Op, 2, V>(in, out, outer, n, inner, (int)k, total, s);
-  if (k <= 4) return go_reg<T, Op, 4, V>(in, out, outer, n, inner, (int)k, total, s);
-  if (k <= 8) return go_reg<T, Op, 8, V>(in, out, outer, n, inner, (int)k, total, s);
+  if (k <= 2) return go_reg<T, Op, 2, V>(in, out, outer, n, inner, (int)k, total, s, ex);
+  if (k <= 4) return go_reg<T, Op, 4, V>(in, out, outer, n, inner, (int)k, total, s, ex);
+  if (k <= 8) return go_reg<T, Op, 8, V>(in, out, outer, n, inner, (int)k, total, s, ex);
   if constexpr (WORDS <= 4) {
-    if (k <= 16) return go_reg<T, Op, 16, V>(in, out, outer, n, inner, (int)k, total, s);
+    if (k <= 16) return go_reg<T, Op, 16, V>(in, out, outer, n, inner, (int)k, total, s, ex);
   }
   if constexpr (WORDS <= 2) {
-    if (k <= 32) return go_reg<T, Op, 32, V>(in, out, outer, n, inner, (int)k, total, s);
+    if (k <= 32) return go_reg<T, Op, 32, V>(in, out, outer, n, inner, (int)k, total, s, ex);
   }
   return -1;  // caller retries with a narrower vector
 }
 
 template <class T, class Op>
 int go_strided(const T* in, T* out, int64_t outer, int64_t n, int64_t inner, int64_t k,
-               const typename AccOf<T>::type* total, cudaStream_t s) {
+               const typename AccOf<T>::type* total, cudaStream_t s, PassExtra* ex) {
   const uintptr_t a = (uintptr_t)in | (uintptr_t)out;
-  const bool v16 = inner % (16 / sizeof(T)) == 0 && a % 16 == 0;  // 16-byte vectors
-  const bool v8 = sizeof(T) == 4 && inner % 2 == 0 && a % 8 == 0;  // 8-byte (float2)
-  if (k > 16 && k <= 32 && sizeof(T) == 8) {
+  // EXSUM_VMAX caps the vector width (measurements); piggy-backed reductions
+  // prefer 8-byte vectors for f32 (half the registers: 2 CTAs per SM)
+  static int vmax = -1;
+  if (vmax < 0) {
+    const char* e = getenv("EXSUM_VMAX");
+    vmax = e ? atoi(e) : 0;
+  }
+  int vcap = vmax > 0 ? vmax : 16;
+  if (vmax == 0 && ex && ex->kind != 0 && sizeof(T) == 4 && k > 8) vcap = 2;
+  const bool v16 = vcap >= (int)(16 / sizeof(T)) && inner % (16 / sizeof(T)) == 0 && a % 16 == 0;
+  const bool v8 = vcap >= 2 && sizeof(T) == 4 && inner % 2 == 0 && a % 8 == 0;  // 8-byte (float2)
+  if (strided_mode() == 4 || (k > 32 && strided_mode() != 1)) {
+    // fall through to the per-block two-sweep kernel below
+  } else if (strided_mode() == 3 || (k > 16 && k <= 32 && sizeof(T) == 8 && strided_mode() != 1)) {
     const int64_t cv = inner;
     const int64_t nb = (n + k - 1) / k;
     const int64_t items = outer * ((cv + 31) / 32) * ((nb + 7) / 8);
@@ -284,11 +395,11 @@ int go_strided(const T* in, T* out, int64_t outer, int64_t n, int64_t inner, int
                                                                      (int)k, total);
     return 1;
   }
-  if (k <= 32) {
+  if (k <= 32 && strided_mode() != 4) {
     int rc = -1;
-    if (v16) rc = go_v<T, Op, 16 / sizeof(T)>(in, out, outer, n, inner, k, total, s);
-    if (rc < 0 && v8) rc = go_v<T, Op, 2>(in, out, outer, n, inner, k, total, s);
-    if (rc < 0) rc = go_v<T, Op, 1>(in, out, outer, n, inner, k, total, s);
+    if (v16) rc = go_v<T, Op, 16 / sizeof(T)>(in, out, outer, n, inner, k, total, s, ex);
+    if (rc < 0 && v8) rc = go_v<T, Op, 2>(in, out, outer, n, inner, k, total, s, ex);
+    if (rc < 0) rc = go_v<T, Op, 1>(in, out, outer, n, inner, k, total, s, ex);
     if (rc >= 0) return rc;
   }
   const int64_t nb = (n + k - 1) / k;
@@ -323,20 +434,46 @@ size_t dtype_size(int dtype) { return dtype == F32 ? 4 : 8; }
 int launch_rows_pass(int dtype, int op, const void* in, void* out, int64_t rows, int64_t n,
                      int64_t k, const void* total, cudaStream_t s);
 
+int launch_strided_bulk(int dtype, int op, const void* in, void* out, int64_t outer, int64_t n,
+                        int64_t inner, int64_t k, const void* total, cudaStream_t s);
+
+// EXSUM_STRIDED=auto|reg|bulk|blockreg|blocks picks the strided kernel (for
+// measurements); auto: register streaming while the register tile fits,
+// the bulk-copy pipeline beyond.
+static int strided_mode() {
+  static int mode = -1;
+  if (mode < 0) {
+    const char* e = getenv("EXSUM_STRIDED");
+    mode = 0;
+    if (e && !strcmp(e, "reg")) mode = 1;
+    if (e && !strcmp(e, "bulk")) mode = 2;
+    if (e && !strcmp(e, "blockreg")) mode = 3;
+    if (e && !strcmp(e, "blocks")) mode = 4;
+  }
+  return mode;
+}
+
 int launch_pass(int dtype, int op, const void* in, void* out, int64_t outer, int64_t n,
-                int64_t inner, int64_t k, const void* total, cudaStream_t s) {
+                int64_t inner, int64_t k, const void* total, cudaStream_t s, PassExtra* ex) {
+  if (ex) ex->done = 0;
   if (inner == 1) return launch_rows_pass(dtype, op, in, out, outer, n, k, total, s);
+  const int mode = strided_mode();
+  const bool big = k > 32 || (dtype != F32 && k > 16);
+  if (mode == 2 || (mode == 0 && big)) {
+    const int rc = launch_strided_bulk(dtype, op, in, out, outer, n, inner, k, total, s);
+    if (rc >= 0) return rc;
+  }
   if (dtype == F32 && op == ADD)
     return go_strided<float, OpAdd>((const float*)in, (float*)out, outer, n, inner, k,
-                                    (const double*)total, s);
+                                    (const double*)total, s, ex);
   if (dtype == F64 && op == ADD)
     return go_strided<double, OpAdd>((const double*)in, (double*)out, outer, n, inner, k,
-                                     (const double*)total, s);
+                                     (const double*)total, s, ex);
   if (dtype == I64 && op == ADD)
     return go_strided<i64, OpAdd>((const i64*)in, (i64*)out, outer, n, inner, k,
-                                  (const i64*)total, s);
+                                  (const i64*)total, s, ex);
   if (dtype == I64 && op == MAX)
-    return go_strided<i64, OpMax>((const i64*)in, (i64*)out, outer, n, inner, k, nullptr, s);
+    return go_strided<i64, OpMax>((const i64*)in, (i64*)out, outer, n, inner, k, nullptr, s, ex);
   return -2;
 }
 

@@ -24,6 +24,7 @@
 namespace exsum {
 
 constexpr int kTotalBlocks = 1184;  // 8 CTAs per SM on 148 SMs; fixed => deterministic
+constexpr int kPartialsCap = 16384;  // capacity of the partials workspace (fused totals)
 
 template <class Acc, class Op>
 __device__ __forceinline__ Acc warp_reduce(Acc v) {
@@ -332,7 +333,50 @@ int go_excl(const T* W, T* out, const T* Tail, int64_t rows, int64_t n, int64_t 
 
 }  // namespace
 
-int reduce_partials_count() { return kTotalBlocks; }
+int reduce_partials_count() { return kPartialsCap; }
+
+// part is [ppr][rows] (written by k_strided_reg<..., EXTRA=1>)
+template <class T, class Op>
+__global__ void k_rowpart_final(const T* __restrict__ part, T* __restrict__ R, int64_t rows,
+                                int64_t ppr) {
+  for (int64_t r = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; r < rows;
+       r += (int64_t)gridDim.x * blockDim.x) {
+    T acc = part[r];
+    for (int64_t i = 1; i < ppr; ++i) acc = Op::apply(acc, part[i * rows + r]);
+    R[r] = acc;
+  }
+}
+
+int launch_rowpart_final(int dtype, int op, const void* part, void* R, int64_t rows, int64_t ppr,
+                         cudaStream_t s) {
+  int64_t grid = (rows + 255) / 256;
+  const int64_t cap = (int64_t)num_sms() * 16;
+  if (grid > cap) grid = cap;
+  if (grid < 1) grid = 1;
+  if (dtype == F32 && op == ADD)
+    k_rowpart_final<float, OpAdd><<<(unsigned)grid, 256, 0, s>>>((const float*)part, (float*)R, rows, ppr);
+  else if (dtype == F64 && op == ADD)
+    k_rowpart_final<double, OpAdd><<<(unsigned)grid, 256, 0, s>>>((const double*)part, (double*)R, rows, ppr);
+  else if (dtype == I64 && op == ADD)
+    k_rowpart_final<i64, OpAdd><<<(unsigned)grid, 256, 0, s>>>((const i64*)part, (i64*)R, rows, ppr);
+  else if (dtype == I64 && op == MAX)
+    k_rowpart_final<i64, OpMax><<<(unsigned)grid, 256, 0, s>>>((const i64*)part, (i64*)R, rows, ppr);
+  else
+    return -2;
+  return 1;
+}
+
+int launch_total_final(int dtype, int op, const void* partials, int64_t np, void* total,
+                       cudaStream_t s) {
+  if (dtype == F32 || dtype == F64) {
+    k_total_final<double, OpAdd><<<1, 1024, 0, s>>>((const double*)partials, (int)np, (double*)total);
+  } else if (op == ADD) {
+    k_total_final<i64, OpAdd><<<1, 1024, 0, s>>>((const i64*)partials, (int)np, (i64*)total);
+  } else {
+    k_total_final<i64, OpMax><<<1, 1024, 0, s>>>((const i64*)partials, (int)np, (i64*)total);
+  }
+  return 1;
+}
 
 int launch_total(int dtype, int op, const void* in, int64_t N, void* partials, void* total,
                  cudaStream_t s) {

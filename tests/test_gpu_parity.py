@@ -121,6 +121,10 @@ EDGE_SHAPES = [
     ((64, 4, 3), (40, 2, 2)), ((5, 6, 7, 5, 6), (4, 4, 4, 4, 4)),
     ((4, 4, 4, 4, 4, 4), (4, 4, 4, 4, 4, 4)), ((3, 5, 2, 7), (1, 1, 1, 1)),
     ((2, 3, 130, 5), (2, 2, 64, 3)),
+    # fused last-two-axes kernel (rows of 256/512/1024, unit tails, segments)
+    ((3, 37, 256), (5, 8, 8)), ((2, 70, 512), (1, 2, 2)), ((2, 70, 512), (3, 16, 16)),
+    ((2, 45, 1024), (2, 16, 16)), ((3, 20, 256), (2, 4, 3)), ((1, 300, 256), (1, 4, 4)),
+    ((1, 130, 1024), (1, 4, 4)), ((2, 19, 512), (1, 8, 5)),
 ]
 
 

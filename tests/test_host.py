@@ -134,7 +134,7 @@ def test_workspace_sizes():
     assert _native.workspace_bytes("bdbs", "float32", "add", (1024, 1024), (1, 16)) == 0
     # box-complement: W buffer + per-level reductions (<= N + small)
     ws = _native.workspace_bytes("box-complement", "float32", "add", (1024,) * 3, (16,) * 3)
-    assert 4 * n <= ws <= 4 * n + 64 * 2**20
+    assert 4 * n <= ws <= 4 * n + 256 * 2**20  # W buffer + row partials + per-level reductions
 
 
 def test_registry_mirrors_reference():
