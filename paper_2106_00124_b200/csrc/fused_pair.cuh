@@ -39,14 +39,14 @@ namespace exsum {
 // K1: window along axis d-2 (compile time); the ROW_WIN row op uses the same
 // window along the row (K2 == K1, the cubic boxes of the BASELINE configs);
 // ROW_EXCL takes any shift kx at run time.
-template <class T, class Op, int C, int K1, int MODE>
-__global__ void __launch_bounds__(32 * C / (16 / sizeof(T)), 1)
+template <class T, class Op, int C, int K1, int MODE, int TV>
+__global__ void __launch_bounds__(32 * C / TV, 1)
 k_fused_pair(const T* __restrict__ in, T* __restrict__ out, int64_t outer, int64_t n1,
              int64_t kx, int64_t seg_len, int64_t nseg,
              const typename AccOf<T>::type* __restrict__ total, const T* __restrict__ Tail) {
-  constexpr int VE = 16 / sizeof(T);
+  constexpr int VE = 16 / sizeof(T);  // 16-byte vector (stage layout, row op)
   constexpr int N2 = 32 * C;           // row length
-  constexpr int NT = N2 / VE;          // threads: one 16-byte column vector each
+  constexpr int NT = N2 / TV;          // threads: one TV-element column vector each
   constexpr int NW = NT / 32;
   constexpr int CV = C / VE;           // vectors per lane chunk
   constexpr int PSV = (CV + 1) | 1;    // padded chunk stride in vectors (odd)
@@ -57,14 +57,15 @@ k_fused_pair(const T* __restrict__ in, T* __restrict__ out, int64_t outer, int64
   constexpr int G = 16 / K1 > 0 ? 16 / K1 : 1;  // blocks per unit
   constexpr int U = G * K1;            // rows per unit: register tile, stage, prefetch granule
   static_assert(C % VE == 0 && (MODE == ROW_EXCL || C % K2 == 0), "shape");
-  typedef Vec<T, VE> VT;
+  typedef Vec<T, VE> VT;  // row-op vectors
+  typedef Vec<T, TV> CT;  // column vectors of the axis-(d-2) pass
   extern __shared__ __align__(16) unsigned char smem[];
   T* raw = reinterpret_cast<T*>(smem);  // [2][U][N2]
   T* wst = raw + 2 * U * N2;            // [U][ROWP]
   const int tid = threadIdx.x;
   const int lane = tid & 31;
   const int warp = tid >> 5;
-  const int col = tid * VE;
+  const int col = tid * TV;
   const int pcol = (col / C) * CH + (col % C);
   const T ident = Op::template identity<T>();
   const T tot = total ? (T)(*total) : T(0);
@@ -93,23 +94,34 @@ k_fused_pair(const T* __restrict__ in, T* __restrict__ out, int64_t outer, int64
     auto issue = [&](int64_t ui) {
       const int rows = rows_of(ui);
       T* d = raw + ((ui - u0) & 1) * (U * N2) + col;
-      for (int r = 0; r < rows; ++r) cp_async16(d + r * N2, src + (ui * U + r) * N2);
+      for (int r = 0; r < rows; ++r) cp_async_n<TV * sizeof(T)>(d + r * N2, src + (ui * U + r) * N2);
       cp_async_commit();  // always commit: uniform group accounting
     };
 
     issue(u0);
     issue(u0 + 1);
     cp_async_wait<1>();
-    VT cur[U];  // raw rows of the current unit
+    CT cur[U];  // raw rows of the current unit
     int len = rows_of(u0);
 #pragma unroll
     for (int r = 0; r < U; ++r)
-      if (r < len) cur[r] = *reinterpret_cast<const VT*>(raw + col + r * N2);
+      if (r < len) cur[r] = *reinterpret_cast<const CT*>(raw + col + r * N2);
     issue(u0 + 2);
 
     for (int64_t u = u0; u < u_end; ++u) {
       const int64_t us = u * U;
       const int rows_u = len;
+      // prefetch this warp's row tails now: they are consumed after the
+      // streaming phase and would otherwise stall the row op on a global load
+      constexpr int RPW = (U + NW - 1) / NW;  // rows per warp in the row op
+      T tails[RPW];
+      if constexpr (MODE == ROW_EXCL) {
+#pragma unroll
+        for (int i = 0; i < RPW; ++i) {
+          const int rr = warp + i * NW;
+          tails[i] = (Tail && rr < rows_u) ? Tail[o * n1 + us + rr] : ident;
+        }
+      }
       if (us + rows_u < n1) cp_async_wait<1>();  // unit u+1 (its first block) has landed
       const T* sn = raw + ((u + 1 - u0) & 1) * (U * N2) + col;
 #pragma unroll
@@ -122,42 +134,42 @@ k_fused_pair(const T* __restrict__ in, T* __restrict__ out, int64_t outer, int64
           for (int r = K1 - 2; r >= 0; --r)
             if (r < blen - 1) {
 #pragma unroll
-              for (int j = 0; j < VE; ++j)
+              for (int j = 0; j < TV; ++j)
                 cur[jb * K1 + r].v[j] = Op::apply(cur[jb * K1 + r].v[j], cur[jb * K1 + r + 1].v[j]);
             }
           if (bs == last_bs) {  // last block of axis d-2: W = S
 #pragma unroll
             for (int r = 0; r < K1; ++r)
-              if (r < blen) *reinterpret_cast<VT*>(wst + (jb * K1 + r) * ROWP + pcol) = cur[jb * K1 + r];
+              if (r < blen) *reinterpret_cast<CT*>(wst + (jb * K1 + r) * ROWP + pcol) = cur[jb * K1 + r];
           } else {
             // stitch with the next block's left-nested prefix (raw)
             const int64_t nrows = n1 - bs - K1;
             const int nlen = (int)(nrows < K1 ? nrows : K1);
-            *reinterpret_cast<VT*>(wst + (jb * K1) * ROWP + pcol) = cur[jb * K1];
+            *reinterpret_cast<CT*>(wst + (jb * K1) * ROWP + pcol) = cur[jb * K1];
             const int nb0 = jb + 1 < G ? (jb + 1) * K1 : 0;  // in range for the dead branch
-            VT P;
+            CT P;
             if (jb + 1 < G) {
               P = cur[nb0];
             } else {
-              P = *reinterpret_cast<const VT*>(sn);
+              P = *reinterpret_cast<const CT*>(sn);
             }
 #pragma unroll
             for (int r = 1; r < K1; ++r) {
               const int jj = r - 1;
               if (jj >= 1 && jj < nlen) {
-                VT a;
+                CT a;
                 if (jb + 1 < G) {
                   a = cur[nb0 + jj];
                 } else {
-                  a = *reinterpret_cast<const VT*>(sn + jj * N2);
+                  a = *reinterpret_cast<const CT*>(sn + jj * N2);
                 }
 #pragma unroll
-                for (int j = 0; j < VE; ++j) P.v[j] = Op::apply(P.v[j], a.v[j]);
+                for (int j = 0; j < TV; ++j) P.v[j] = Op::apply(P.v[j], a.v[j]);
               }
-              VT w;
+              CT w;
 #pragma unroll
-              for (int j = 0; j < VE; ++j) w.v[j] = Op::apply(cur[jb * K1 + r].v[j], P.v[j]);
-              *reinterpret_cast<VT*>(wst + (jb * K1 + r) * ROWP + pcol) = w;
+              for (int j = 0; j < TV; ++j) w.v[j] = Op::apply(cur[jb * K1 + r].v[j], P.v[j]);
+              *reinterpret_cast<CT*>(wst + (jb * K1 + r) * ROWP + pcol) = w;
             }
           }
         }
@@ -167,13 +179,16 @@ k_fused_pair(const T* __restrict__ in, T* __restrict__ out, int64_t outer, int64
       if (u + 1 < u_end) {
 #pragma unroll
         for (int r = 0; r < U; ++r)
-          if (r < len) cur[r] = *reinterpret_cast<const VT*>(sn + r * N2);
+          if (r < len) cur[r] = *reinterpret_cast<const CT*>(sn + r * N2);
       }
       issue(u + 3);
       __syncthreads();
 
       // ---- row operation on the rows_u rows of the stage (warp per row) ----
-      for (int rr = warp; rr < rows_u; rr += NW) {
+#pragma unroll
+      for (int ri = 0; ri < RPW; ++ri) {
+        const int rr = warp + ri * NW;
+        if (rr >= rows_u) break;
         T* wrow = wst + rr * ROWP;
         T* mine = wrow + lane * CH;
         T a[C];
@@ -257,7 +272,7 @@ k_fused_pair(const T* __restrict__ in, T* __restrict__ out, int64_t outer, int64
             }
           }
           __syncwarp();
-          const T tail = Tail ? Tail[o * n1 + us + rr] : ident;
+          const T tail = tails[ri];
           T pe = pre;
           if (kvec) {
             // the shift keeps vector alignment: S[x+k] read as 16-byte vectors
@@ -301,18 +316,26 @@ k_fused_pair(const T* __restrict__ in, T* __restrict__ out, int64_t outer, int64
       }
       __syncthreads();
       for (int r = 0; r < rows_u; ++r)
-        st_stream<T, VE>(dst + (us + r) * N2, *reinterpret_cast<const VT*>(wst + r * ROWP + pcol));
+        st_stream<T, TV>(dst + (us + r) * N2, *reinterpret_cast<const CT*>(wst + r * ROWP + pcol));
     }
     cp_async_wait<0>();
   }
+}
+
+// threads own TV-element column vectors: ~256-512 threads per CTA
+template <class T, int C>
+constexpr int pick_tv() {
+  return (32 * C) / (16 / (int)sizeof(T)) >= 256 ? ((32 * C) / 512 >= 1 ? (32 * C) / 512 : 1)
+                                                 : (32 * C) / 256 >= 1 ? (32 * C) / 256 : 1;
 }
 
 template <class T, class Op, int C, int K1, int MODE>
 int go_pair(const T* in, T* out, int64_t outer, int64_t n1, int64_t kx,
             const typename AccOf<T>::type* total, const T* Tail, cudaStream_t s) {
   constexpr int VE = 16 / sizeof(T);
+  constexpr int TV = VE;  // 16-byte column vectors measured best (8-byte: -30% at C4)
   constexpr int N2 = 32 * C;
-  constexpr int NT = N2 / VE;
+  constexpr int NT = N2 / TV;
   constexpr int CV = C / VE;
   constexpr int PSV = (CV + 1) | 1;
   constexpr int ROWP = 32 * PSV * VE;
@@ -336,10 +359,10 @@ int go_pair(const T* in, T* out, int64_t outer, int64_t n1, int64_t kx,
   int64_t grid = items;
   const int64_t cap = (int64_t)num_sms() * per_sm * 4;
   if (grid > cap) grid = cap;
-  cudaFuncSetAttribute(k_fused_pair<T, Op, C, K1, MODE>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                       (int)smem);
-  k_fused_pair<T, Op, C, K1, MODE><<<(unsigned)grid, NT, smem, s>>>(in, out, outer, n1, kx, seg_len,
-                                                                   nseg, total, Tail);
+  cudaFuncSetAttribute(k_fused_pair<T, Op, C, K1, MODE, TV>,
+                       cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  k_fused_pair<T, Op, C, K1, MODE, TV><<<(unsigned)grid, NT, smem, s>>>(in, out, outer, n1, kx,
+                                                                       seg_len, nseg, total, Tail);
   return 1;
 }
 
