@@ -66,13 +66,14 @@ class ClockSampler:
     def __init__(self, index: int):
         self.index = index
         self.proc = None
-        self.lines = []
+        self.lines = []  # (wall time, csv line)
+        self.window = None
 
     def __enter__(self):
         try:
             self.proc = subprocess.Popen(
                 ["nvidia-smi", "-i", str(self.index), f"--query-gpu={self.FIELDS}",
-                 "--format=csv,noheader,nounits", "-lms", "100"],
+                 "--format=csv,noheader,nounits", "-lms", "20"],
                 stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
             self.thread = threading.Thread(target=self._read, daemon=True)
             self.thread.start()
@@ -82,7 +83,11 @@ class ClockSampler:
 
     def _read(self):
         for line in self.proc.stdout:
-            self.lines.append(line.strip())
+            self.lines.append((time.time(), line.strip()))
+
+    def mark(self, t0, t1):
+        """The timed region [t0, t1] (wall clock)."""
+        self.window = (t0, t1)
 
     def __exit__(self, *exc):
         if self.proc is not None:
@@ -95,7 +100,18 @@ class ClockSampler:
     def summary(self):
         sms, mx, reasons = [], None, set()
         names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
-        for ln in self.lines:
+        lines = self.lines
+        scope = "timed region"
+        if self.window is not None:
+            t0, t1 = self.window
+            inside = [ln for t, ln in lines if t0 <= t <= t1]
+            if len(inside) < 3:  # a short region: widen to the loaded window around it
+                inside = [ln for t, ln in lines if t0 - 1.0 <= t <= t1 + 0.2]
+                scope = "timed region +-1 s (loaded: warm-up and timed steps)"
+            lines = inside
+        else:
+            lines = [ln for _, ln in lines]
+        for ln in lines:
             parts = [p.strip() for p in ln.split(",")]
             if len(parts) < 6:
                 continue
@@ -110,7 +126,7 @@ class ClockSampler:
         if not sms:
             return {"sm_mhz": None, "sm_max_mhz": None, "reasons": [], "samples": 0}
         return {"sm_mhz": statistics.median(sms), "sm_max_mhz": mx, "reasons": sorted(reasons),
-                "samples": len(sms)}
+                "samples": len(sms), "scope": scope}
 
 
 def make_input(cfg, device, seed=0, shape=None):
@@ -244,6 +260,8 @@ def main():
         step = lambda: fn(t, box)  # noqa: E731
 
     stream = torch.cuda.current_stream(dev)
+    clocks = ClockSampler(local).__enter__()
+    time.sleep(0.5)  # let nvidia-smi start sampling
     for _ in range(args.warmup):
         out = step()
     torch.cuda.synchronize(dev)
@@ -257,14 +275,17 @@ def main():
     if dist is not None:
         dist.barrier()
     torch.cuda.synchronize(dev)
-    with ClockSampler(local) as clocks:
-        for i in range(args.steps):
-            starts[i].record(stream)
-            out = step()
-            ends[i].record(stream)
-            launches += _native.last_launch_count()
-            del out
-        torch.cuda.synchronize(dev)
+    t_begin = time.time()
+    for i in range(args.steps):
+        starts[i].record(stream)
+        out = step()
+        ends[i].record(stream)
+        launches += _native.last_launch_count()
+        del out
+    torch.cuda.synchronize(dev)
+    clocks.mark(t_begin, time.time())
+    time.sleep(0.1)
+    clocks.__exit__(None, None, None)
     if dist is not None:
         dist.barrier()
     step_ms = [s.elapsed_time(e) for s, e in zip(starts, ends)]
@@ -282,7 +303,8 @@ def main():
     peak, peak_kind = _peaks()
     per = {}
     for name, b, ms in prof:
-        d = per.setdefault(name, {"ms": 0.0, "bytes": 0.0, "launches": 0})
+        key = f"{name}[{b / 2**20:.0f}MiB]"
+        d = per.setdefault(key, {"ms": 0.0, "bytes": 0.0, "launches": 0})
         d["ms"] += ms
         d["bytes"] += b
         d["launches"] += 1
@@ -386,10 +408,12 @@ def main():
 
 
 def _ncu_traffic(kernel):
-    """dram bytes per launch of `kernel` from the committed ncu summary, if any."""
+    """dram__bytes_read.sum + dram__bytes_write.sum per launch of `kernel`, from
+    the committed ncu --set full capture (profiles/ncu_traffic.json), if any."""
     try:
         with open(os.path.join(ROOT, "profiles", "ncu_traffic.json")) as f:
-            return json.load(f).get(kernel)
+            rec = json.load(f).get(kernel)
+        return rec["dram_bytes_per_launch"] if rec else None
     except Exception:
         return None
 
