@@ -251,7 +251,7 @@ def main():
         from paper_2106_00124_b200 import sharded
 
         x = sharded.make_local_slab(lambda shape: make_input(args.config, dev, shape=shape),
-                                    ext, rank, world)
+                                    ext, rank, world, box)
         runner = sharded.ShardedRunner(args.route, ops, ext, box, rank, world, dev)
         step = lambda: runner(x)  # noqa: E731
     else:

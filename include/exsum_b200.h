@@ -115,6 +115,33 @@ int exsum_profile_enable(int on);
 int exsum_profile_count(void);
 int exsum_profile_get(int i, char *name, int name_len, double *bytes, float *ms);
 
+/* ---- axis-0 sharding stages (multi-GPU; no NCCL inside) ----
+ * A rank owns planes [x_s, x_e) of axis 0 (x_s a multiple of box[0]) and holds
+ * the next rank's first box[0]-1 planes as a halo right after them.
+ *
+ * exsum_shard_axis0_pass: the axis-0 windowed pass of own+halo planes
+ *   (ext_in[0] = own + halo) producing only the n_out own planes; extra_kind
+ *   1 also writes R (fold over the last axis of the own raw planes,
+ *   n_out*prod(ext[1:d-1]) elements), 2 the local total (one double for
+ *   float types, one int64 for add-i64) into extra_out.
+ * exsum_bdbs_finish: the remaining windowed passes (axes 1..d-1) of a shard;
+ *   total != NULL (device, the global total) applies the BDBSC complement.
+ * exsum_box_complement_finish: the remaining W passes (axes 1..d-2) and the
+ *   last-axis round with the tail slice (device, one value per own row). */
+int exsum_shard_workspace_bytes(int stage, int dtype, int op, int d, const int64_t *ext,
+                                const int64_t *box, int64_t n_out, int extra_kind,
+                                size_t *bytes);
+int exsum_shard_axis0_pass(const void *in, void *out, int dtype, int op, int d,
+                           const int64_t *ext_in, const int64_t *box, int64_t n_out,
+                           int extra_kind, void *extra_out, void *ws, size_t ws_bytes,
+                           void *stream);
+int exsum_bdbs_finish(const void *in, void *out, int dtype, int op, int d, const int64_t *ext,
+                      const int64_t *box, const void *total, void *ws, size_t ws_bytes,
+                      void *stream);
+int exsum_box_complement_finish(const void *in, void *out, int dtype, int op, int d,
+                                const int64_t *ext, const int64_t *box, const void *tail,
+                                void *ws, size_t ws_bytes, void *stream);
+
 #ifdef __cplusplus
 }
 #endif

@@ -35,6 +35,10 @@ EXPORTS = (
     "exsum_profile_enable",
     "exsum_profile_count",
     "exsum_profile_get",
+    "exsum_shard_workspace_bytes",
+    "exsum_shard_axis0_pass",
+    "exsum_bdbs_finish",
+    "exsum_box_complement_finish",
 )
 
 _lock = threading.Lock()
@@ -76,6 +80,16 @@ def load():
         L.exsum_profile_get.argtypes = [ci, ctypes.c_char_p, ci, ctypes.POINTER(ctypes.c_double),
                                         ctypes.POINTER(ctypes.c_float)]
         L.exsum_profile_get.restype = ci
+        L.exsum_shard_workspace_bytes.argtypes = [ci, ci, ci, ci, i64p, i64p, ctypes.c_int64, ci,
+                                                  ctypes.POINTER(sz)]
+        L.exsum_shard_workspace_bytes.restype = ci
+        L.exsum_shard_axis0_pass.argtypes = [vp, vp, ci, ci, ci, i64p, i64p, ctypes.c_int64, ci, vp,
+                                             vp, sz, vp]
+        L.exsum_shard_axis0_pass.restype = ci
+        for name in ("exsum_bdbs_finish", "exsum_box_complement_finish"):
+            fn = getattr(L, name)
+            fn.argtypes = [vp, vp, ci, ci, ci, i64p, i64p, vp, vp, sz, vp]
+            fn.restype = ci
         if L.exsum_abi_version() != 1:
             raise DeviceError("libexsum_b200.so ABI version mismatch")
         _lib = L

@@ -198,7 +198,8 @@ int no_hook() { return EXSUM_OK; }
 // ------------------------------------------------------------------ routes --
 
 int route_bdbs(const Shape& s, int dtype, int op, const void* in, void* out, Arena& ar,
-               bool complement, cudaStream_t st, int* launches) {
+               bool complement, cudaStream_t st, int* launches,
+               const void* given_total = nullptr) {
   const size_t es = dtype_size(dtype);
   const bool live = ar.base != nullptr;
   PassPlan p = plan_passes(s, s.d);
@@ -209,8 +210,9 @@ int route_bdbs(const Shape& s, int dtype, int op, const void* in, void* out, Are
     total = ar.take(8);
   }
   void* other = p.count >= 2 ? ar.take((size_t)s.N * es) : nullptr;
+  if (given_total) total = const_cast<void*>(given_total);  // shard: the global total
   auto full_total = [&]() {
-    if (live) {
+    if (live && !given_total) {
       ProfScope ps("total", (double)s.N * es, st);
       *launches += launch_total(dtype, op, in, s.N, partials, total, st);
     }
@@ -236,7 +238,7 @@ int route_bdbs(const Shape& s, int dtype, int op, const void* in, void* out, Are
   ex0.kind = 2;
   ex0.buf = partials;
   ex0.cap = reduce_partials_count();
-  const bool piggy = complement && head.count >= 1 && (fused || head.count >= 2);
+  const bool piggy = complement && !given_total && head.count >= 1 && (fused || head.count >= 2);
   if (complement && !piggy) full_total();
   auto finish_total = [&]() -> int {
     if (piggy && live) {
@@ -264,6 +266,50 @@ int route_bdbs(const Shape& s, int dtype, int op, const void* in, void* out, Are
                                s.k[d - 1], ROW_WIN, total, nullptr, st);
     if (rc < 0) return fail(EXSUM_ECUDA, "fused pass pair failed to launch");
     *launches += rc;
+  }
+  return EXSUM_OK;
+}
+
+// The box-complement round after R/T are known: W passes along `head` (the
+// first one may carry the R reduction, ex0, with hook() right after it),
+// then the row round with tail T, fused with the last W pass when `fused`.
+template <class F>
+int bc_finish(const Shape& s, int dtype, int op, const void* src, void* dst, const void* T,
+              const PassPlan& head, bool fused, PassExtra* ex0, F hook, Arena& ar,
+              cudaStream_t st, int* launches) {
+  const size_t es = dtype_size(dtype);
+  const bool live = ar.base != nullptr;
+  const int d = s.d;
+  const int64_t n = s.ext[d - 1];
+  const int64_t rows = s.N / n;
+  const void* W = src;
+  if (head.count > 0) {
+    void* wbuf = ar.take((size_t)s.N * es);
+    // the chain ends in wbuf; dst serves as the ping-pong partner
+    int rc = run_chain(s, head, dtype, op, src, wbuf, dst, nullptr, st, launches, live, ex0,
+                       hook);
+    if (rc) return rc;
+    W = wbuf;
+  } else {
+    int rc = hook();
+    if (rc) return rc;
+  }
+  if (fused) {
+    // last W pass (axis d-2) fused with the row round (fused_pair.cu)
+    if (live) {
+      ProfScope ps("fused_pair", (double)(2 * s.N + rows) * es, st);
+      const int64_t n1 = s.ext[d - 2];
+      int rc = launch_fused_pair(dtype, op, W, dst, s.N / (n1 * n), n1, n, s.k[d - 2], s.k[d - 1],
+                                 ROW_EXCL, nullptr, T, st);
+      if (rc < 0) return fail(EXSUM_ECUDA, "fused pass pair failed to launch");
+      *launches += rc;
+    }
+    return EXSUM_OK;
+  }
+  void* scratch = ar.take(excl_rows_scratch_elems(dtype, rows, n) * es);
+  if (live) {
+    ProfScope ps("excl_rows", (double)(2 * s.N + rows) * es, st);
+    *launches += launch_excl_rows(dtype, op, W, dst, T, rows, n, s.k[d - 1], scratch, st);
   }
   return EXSUM_OK;
 }
@@ -315,36 +361,7 @@ int route_box_complement(const Shape& s, int dtype, int op, const void* src, voi
     }
     return route_box_complement(t, dtype, op, R, T, ar, st, launches);
   };
-  const void* W = src;
-  if (head.count > 0) {
-    void* wbuf = ar.take((size_t)s.N * es);
-    // the chain ends in wbuf; dst serves as the ping-pong partner
-    int rc = run_chain(s, head, dtype, op, src, wbuf, dst, nullptr, st, launches, live, &ex0,
-                       reduce_and_tail);
-    if (rc) return rc;
-    W = wbuf;
-  } else {
-    int rc = reduce_and_tail();
-    if (rc) return rc;
-  }
-  if (fused) {
-    // last W pass (axis d-2) fused with the row round (fused_pair.cu)
-    if (live) {
-      ProfScope ps("fused_pair", (double)(2 * s.N + rows) * es, st);
-      const int64_t n1 = s.ext[d - 2];
-      int rc = launch_fused_pair(dtype, op, W, dst, s.N / (n1 * n), n1, n, s.k[d - 2], s.k[d - 1],
-                                 ROW_EXCL, nullptr, T, st);
-      if (rc < 0) return fail(EXSUM_ECUDA, "fused pass pair failed to launch");
-      *launches += rc;
-    }
-    return EXSUM_OK;
-  }
-  void* scratch = ar.take(excl_rows_scratch_elems(dtype, rows, n) * es);
-  if (live) {
-    ProfScope ps("excl_rows", (double)(2 * s.N + rows) * es, st);
-    *launches += launch_excl_rows(dtype, op, W, dst, T, rows, n, s.k[d - 1], scratch, st);
-  }
-  return EXSUM_OK;
+  return bc_finish(s, dtype, op, src, dst, T, head, fused, &ex0, reduce_and_tail, ar, st, launches);
 }
 
 int dispatch(int route, const Shape& s, int dtype, int op, const void* in, void* out, Arena& ar,
@@ -390,6 +407,134 @@ int run_device(int route, const void* in, void* out, int dtype, int op, int d, c
   Arena ar(ws);
   launches = 0;
   rc = dispatch(route, s, dtype, op, in, out, ar, (cudaStream_t)stream, &launches);
+  if (rc) return rc;
+  g_last_launches = launches;
+  return cuda_check("kernel launch");
+}
+
+
+// ----------------------------------------------------- shard stages (8e) --
+// Axis-0 sharding (paper_2106_00124_b200/sharded.py): a rank owns planes
+// [x_s, x_e) of axis 0 and receives the next rank's first k0-1 planes as a
+// halo.  Stage 1 runs the axis-0 windowed pass over own+halo planes producing
+// only the own planes (optionally folding the raw own planes into R or the
+// local total); stage 2 finishes BDBS/BDBSC (remaining axes, global total) or
+// box-complement (remaining W passes + row round with the tail slice).
+
+int stage_axis0(const Shape& s, int64_t n_out, int64_t k0, int dtype, int op, const void* in,
+                void* out, int extra_kind, void* extra_out, Arena& ar, cudaStream_t st,
+                int* launches) {
+  const size_t es = dtype_size(dtype);
+  const bool live = ar.base != nullptr;
+  const int d = s.d;
+  const int64_t n_in = s.ext[0];
+  const int64_t inner = s.N / n_in;
+  const int64_t N_out = n_out * inner;
+  const int64_t row_len = s.ext[d - 1];
+  const int64_t rows_out = N_out / row_len;
+  const int64_t k = k0 < n_in ? k0 : n_in;
+  void* partials = ar.take((size_t)reduce_partials_count() * 8);
+  void* rowpart = extra_kind == 1 ? ar.take((size_t)(N_out / 32 + 1) * es) : nullptr;
+  void* tmp = (k > 1 && n_out != n_in) ? ar.take((size_t)s.N * es) : nullptr;
+  if (!live) return EXSUM_OK;
+  PassExtra ex;
+  bool extras_done = false;
+  if (k == 1) {
+    cudaMemcpyAsync(out, in, (size_t)N_out * es, cudaMemcpyDeviceToDevice, st);
+  } else {
+    ex.kind = extra_kind;
+    ex.buf = extra_kind == 1 ? rowpart : partials;
+    ex.row_len = row_len;
+    ex.cap = reduce_partials_count();
+    ex.n_out = n_out == n_in ? -1 : n_out;
+    {
+      ProfScope ps("shard_axis0", (double)(n_in * inner + N_out) * es, st);
+      int rc = launch_pass(dtype, op, in, out, 1, n_in, inner, k, nullptr, st, &ex);
+      if (rc < 0) return fail(EXSUM_ECONFIG, "no kernel for this dtype/operator");
+      *launches += rc;
+    }
+    if (ex.n_out >= 0 && !ex.n_out_done) {
+      // the pass kernel for this shape cannot stop at n_out: full-length pass
+      // into a temporary, then keep the own planes
+      PassExtra plain;
+      int rc = launch_pass(dtype, op, in, tmp, 1, n_in, inner, k, nullptr, st, &plain);
+      if (rc < 0) return fail(EXSUM_ECONFIG, "no kernel for this dtype/operator");
+      *launches += rc;
+      cudaMemcpyAsync(out, tmp, (size_t)N_out * es, cudaMemcpyDeviceToDevice, st);
+    } else {
+      extras_done = ex.done != 0;
+    }
+  }
+  if (extra_kind == 1) {
+    if (extras_done)
+      *launches += launch_rowpart_final(dtype, op, rowpart, extra_out, rows_out, ex.ppr, st);
+    else
+      *launches += launch_row_reduce(dtype, op, in, extra_out, rows_out, row_len, st);
+  } else if (extra_kind == 2) {
+    if (extras_done)
+      *launches += launch_total_final(dtype, op, partials, ex.ppr, extra_out, st);
+    else
+      *launches += launch_total(dtype, op, in, N_out, partials, extra_out, st);
+  }
+  return EXSUM_OK;
+}
+
+int stage_bc_finish(const Shape& s, int dtype, int op, const void* in, void* out, const void* T,
+                    Arena& ar, cudaStream_t st, int* launches) {
+  const int d = s.d;
+  PassPlan p = plan_passes(s, d - 1);
+  PassPlan head;  // axis 0 was done by stage 1
+  for (int i = 0; i < p.count; ++i)
+    if (p.axes[i] != 0) head.axes[head.count++] = p.axes[i];
+  const bool fused = head.count > 0 && head.axes[head.count - 1] == d - 2 &&
+                     fused_pair_ok(dtype, op, s.ext[d - 1], s.k[d - 2], s.k[d - 1], ROW_EXCL);
+  if (fused) head.count -= 1;
+  return bc_finish(s, dtype, op, in, out, T, head, fused, nullptr, no_hook, ar, st, launches);
+}
+
+// stage 0: axis-0 shard pass; 1: bdbs/bdbsc finish; 2: box-complement finish
+int run_stage(int stage, int dtype, int op, int d, const int64_t* ext, const int64_t* box,
+              int64_t n_out, int extra_kind, const void* in, void* out, const void* aux,
+              void* extra_out, Arena& ar, cudaStream_t st, int* launches) {
+  Shape s;
+  int rc = check_types(dtype, op);
+  if (rc) return rc;
+  rc = normalize(d, ext, box, &s);
+  if (rc) return rc;
+  if (stage == 0) {
+    if (n_out < 1 || n_out > s.ext[0]) return fail(EXSUM_EUSAGE, "n_out must be in [1, ext[0]]");
+    if (n_out != s.ext[0] && box[0] > 1 && n_out % box[0] != 0)
+      return fail(EXSUM_EUSAGE, "a shard's own planes must be a multiple of the axis-0 window");
+    if (extra_kind < 0 || extra_kind > 2) return fail(EXSUM_EUSAGE, "extra_kind must be 0, 1 or 2");
+    if (extra_kind == 2 && op == EXSUM_MAX) return fail(EXSUM_ECONFIG, "no total for max-i64 (bdbsc needs an inverse)");
+    return stage_axis0(s, n_out, box[0], dtype, op, in, out, extra_kind, extra_out, ar, st, launches);
+  }
+  s.k[0] = 1;
+  if (stage == 1) return route_bdbs(s, dtype, op, in, out, ar, aux != nullptr, st, launches, aux);
+  if (stage == 2) {
+    if (d < 2) return fail(EXSUM_ECONFIG, "sharded box-complement needs d >= 2");
+    s.k[0] = box[0] < ext[0] ? box[0] : ext[0];
+    return stage_bc_finish(s, dtype, op, in, out, aux, ar, st, launches);
+  }
+  return fail(EXSUM_EUSAGE, "unknown stage");
+}
+
+int run_stage_device(int stage, int dtype, int op, int d, const int64_t* ext, const int64_t* box,
+                     int64_t n_out, int extra_kind, const void* in, void* out, const void* aux,
+                     void* extra_out, void* ws, size_t ws_bytes, void* stream) {
+  g_err.clear();
+  if (!in || !out || in == out) return fail(EXSUM_EUSAGE, "need distinct in/out");
+  Arena sizing(nullptr);
+  int launches = 0;
+  int rc = run_stage(stage, dtype, op, d, ext, box, n_out, extra_kind, in, out, aux, extra_out,
+                     sizing, (cudaStream_t)stream, &launches);
+  if (rc) return rc;
+  if (sizing.off > 0 && (ws == nullptr || ws_bytes < sizing.off))
+    return fail(EXSUM_EUSAGE, "workspace too small (see exsum_shard_workspace_bytes)");
+  Arena ar(ws);
+  launches = 0;
+  rc = run_stage(stage, dtype, op, d, ext, box, n_out, extra_kind, in, out, aux, extra_out, ar,
+                 (cudaStream_t)stream, &launches);
   if (rc) return rc;
   g_last_launches = launches;
   return cuda_check("kernel launch");
@@ -555,6 +700,44 @@ int exsum_profile_get(int i, char* name, int name_len, double* bytes, float* ms)
     *ms = v;
   }
   return EXSUM_OK;
+}
+
+int exsum_shard_workspace_bytes(int stage, int dtype, int op, int d, const int64_t* ext,
+                                const int64_t* box, int64_t n_out, int extra_kind,
+                                size_t* bytes) {
+  g_err.clear();
+  Arena sizing(nullptr);
+  int launches = 0;
+  int rc = run_stage(stage, dtype, op, d, ext, box, n_out, extra_kind, (const void*)1, (void*)2,
+                     (const void*)3, (void*)4, sizing, nullptr, &launches);
+  if (rc) return rc;
+  if (bytes) *bytes = sizing.off;
+  return EXSUM_OK;
+}
+
+int exsum_shard_axis0_pass(const void* in, void* out, int dtype, int op, int d,
+                           const int64_t* ext_in, const int64_t* box, int64_t n_out,
+                           int extra_kind, void* extra_out, void* ws, size_t ws_bytes,
+                           void* stream) {
+  if (extra_kind != 0 && !extra_out) return fail(EXSUM_EUSAGE, "extra_out is required");
+  return run_stage_device(0, dtype, op, d, ext_in, box, n_out, extra_kind, in, out, nullptr,
+                          extra_out, ws, ws_bytes, stream);
+}
+
+int exsum_bdbs_finish(const void* in, void* out, int dtype, int op, int d, const int64_t* ext,
+                      const int64_t* box, const void* total, void* ws, size_t ws_bytes,
+                      void* stream) {
+  if (total && op == EXSUM_MAX) return fail(EXSUM_ECONFIG, "bdbsc requires an invertible monoid");
+  return run_stage_device(1, dtype, op, d, ext, box, 0, 0, in, out, total, nullptr, ws, ws_bytes,
+                          stream);
+}
+
+int exsum_box_complement_finish(const void* in, void* out, int dtype, int op, int d,
+                                const int64_t* ext, const int64_t* box, const void* tail,
+                                void* ws, size_t ws_bytes, void* stream) {
+  if (!tail) return fail(EXSUM_EUSAGE, "tail is required");
+  return run_stage_device(2, dtype, op, d, ext, box, 0, 0, in, out, tail, nullptr, ws, ws_bytes,
+                          stream);
 }
 
 int exsum_release_cache(void) {

@@ -26,6 +26,9 @@ enum OpCode { ADD = 0, MAX = 1 };
 //           launch_rowpart_final);
 //   kind 2: per-CTA partial totals into buf (capacity cap); on success ppr =
 //           number of partials (finish with launch_total_final).
+// n_out >= 0: produce only rows [0, n_out) along the axis (the output has
+// n_out rows; outer must be 1) -- a shard reading a halo beyond its planes;
+// n_out_done reports whether the launched kernel honoured it.
 struct PassExtra {
   int kind = 0;
   void* buf = nullptr;
@@ -33,6 +36,8 @@ struct PassExtra {
   int64_t cap = 0;
   int done = 0;
   int64_t ppr = 0;
+  int64_t n_out = -1;
+  int n_out_done = 0;
 };
 
 int launch_pass(int dtype, int op, const void* in, void* out, int64_t outer, int64_t n,

@@ -41,9 +41,13 @@ __global__ void __launch_bounds__(256)
 k_strided_reg(const T* __restrict__ in, T* __restrict__ out, int64_t outer, int64_t n,
               int64_t inner, int k, int64_t seg_len, int64_t nseg,
               const typename AccOf<T>::type* __restrict__ total, T* __restrict__ rowpart = nullptr,
-              int64_t row_len = 0, typename AccOf<T>::type* __restrict__ tpart = nullptr) {
+              int64_t row_len = 0, typename AccOf<T>::type* __restrict__ tpart = nullptr,
+              int64_t n_out = -1) {
   typedef Vec<T, V> VT;
   typedef typename AccOf<T>::type Acc;
+  // rows produced along the axis: [0, nout) (a shard's own planes when the
+  // input carries a halo of the next shard's planes beyond them)
+  const int64_t nout = n_out < 0 ? n : n_out;
   Acc tacc[V];
 #pragma unroll
   for (int j = 0; j < V; ++j) tacc[j] = Op::template identity<Acc>();
@@ -82,7 +86,7 @@ k_strided_reg(const T* __restrict__ in, T* __restrict__ out, int64_t outer, int6
       if ((lane & (LOWB - 1)) == 0 && rowbase < nrows) {
         const int64_t c0 = c - lane;  // the warp's first column vector
         const int64_t e = (o * n + x0 + rowbase) * inner + c0 * V;
-        const int64_t rows_total = outer * n * inner / row_len;
+        const int64_t rows_total = outer * nout * inner / row_len;
         rowpart[((e % row_len) / (32 * V)) * rows_total + e / row_len] = sv[0];
       }
     } else if constexpr (EXTRA == 2) {
@@ -107,9 +111,9 @@ k_strided_reg(const T* __restrict__ in, T* __restrict__ out, int64_t outer, int6
     const int64_t o = rest % outer;
     const int64_t seg = rest / outer;
     const int64_t xs = seg * seg_len;
-    const int64_t xe = xs + seg_len < n ? xs + seg_len : n;
+    const int64_t xe = xs + seg_len < nout ? xs + seg_len : nout;
     const T* pin = in + o * n * inner + c * V;
-    T* pout = out + o * n * inner + c * V;
+    T* pout = out + o * nout * inner + c * V;
 
     VT cur[KMAX];
     int64_t bs = xs;
@@ -309,12 +313,13 @@ int g_num_sms = 0;
 template <class T, class Op, int KMAX, int V>
 int go_reg(const T* in, T* out, int64_t outer, int64_t n, int64_t inner, int k,
            const typename AccOf<T>::type* total, cudaStream_t s, PassExtra* ex) {
+  const int64_t nout = (ex && ex->n_out >= 0) ? ex->n_out : n;
   const int64_t lines = outer * (inner / V);
   // split the axis into k-aligned segments until ~2 waves of 256-thread
   // blocks are resident; keep segments >= 16 blocks so the halo stays small
   const int64_t want_threads = (int64_t)num_sms() * 1536;
   int64_t nseg = (want_threads + lines - 1) / lines;
-  const int64_t nblocks = (n + k - 1) / k;
+  const int64_t nblocks = (nout + k - 1) / k;
   // halo cost is one block per segment: keep >= 16 blocks per segment for
   // arrays that stream from HBM, but go down to 2 for L2-resident ones (there
   // the kernel is latency bound and parallelism wins)
@@ -324,28 +329,30 @@ int go_reg(const T* in, T* out, int64_t outer, int64_t n, int64_t inner, int k,
   if (nseg > max_seg) nseg = max_seg;
   if (nseg < 1) nseg = 1;
   const int64_t seg_len = (int64_t)k * ((nblocks + nseg - 1) / nseg);
-  nseg = (n + seg_len - 1) / seg_len;
+  nseg = (nout + seg_len - 1) / seg_len;
   const int64_t items = lines * nseg;
   int64_t grid = (items + 255) / 256;
   const int64_t cap = (int64_t)num_sms() * 64;
   if (grid > cap) grid = cap;
   typedef typename AccOf<T>::type Acc;
+  if (ex) ex->n_out_done = 1;
   if (ex && ex->kind == 1 && ex->row_len % (32 * V) == 0 && (inner / V) % 32 == 0) {
     k_strided_reg<T, Op, KMAX, V, 1><<<(unsigned)grid, 256, 0, s>>>(
-        in, out, outer, n, inner, k, seg_len, nseg, total, (T*)ex->buf, ex->row_len, nullptr);
+        in, out, outer, n, inner, k, seg_len, nseg, total, (T*)ex->buf, ex->row_len, nullptr, nout);
     ex->done = 1;
     ex->ppr = ex->row_len / (32 * V);
     return 1;
   }
   if (ex && ex->kind == 2 && grid <= ex->cap) {
     k_strided_reg<T, Op, KMAX, V, 2><<<(unsigned)grid, 256, 0, s>>>(
-        in, out, outer, n, inner, k, seg_len, nseg, total, nullptr, 0, (Acc*)ex->buf);
+        in, out, outer, n, inner, k, seg_len, nseg, total, nullptr, 0, (Acc*)ex->buf, nout);
     ex->done = 1;
     ex->ppr = grid;
     return 1;
   }
   k_strided_reg<T, Op, KMAX, V><<<(unsigned)grid, 256, 0, s>>>(in, out, outer, n, inner, k,
-                                                               seg_len, nseg, total);
+                                                               seg_len, nseg, total, nullptr, 0,
+                                                               nullptr, nout);
   return 1;
 }
 
@@ -455,7 +462,15 @@ static int strided_mode() {
 
 int launch_pass(int dtype, int op, const void* in, void* out, int64_t outer, int64_t n,
                 int64_t inner, int64_t k, const void* total, cudaStream_t s, PassExtra* ex) {
-  if (ex) ex->done = 0;
+  if (ex) {
+    ex->done = 0;
+    ex->n_out_done = 0;
+  }
+  if (ex && ex->n_out >= 0 && ex->n_out != n) {
+    // a shard pass producing fewer rows than it reads: register streaming only
+    // (callers fall back to a full-length pass into a temporary otherwise)
+    if (inner == 1 || k > 32 || (dtype != F32 && k > 16)) return 0;
+  }
   if (inner == 1) return launch_rows_pass(dtype, op, in, out, outer, n, k, total, s);
   const int mode = strided_mode();
   const bool big = k > 32 || (dtype != F32 && k > 16);
