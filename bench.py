@@ -276,12 +276,13 @@ def main():
         dist.barrier()
     torch.cuda.synchronize(dev)
     t_begin = time.time()
+    launches0 = _native.total_launch_count()
     for i in range(args.steps):
         starts[i].record(stream)
         out = step()
         ends[i].record(stream)
-        launches += _native.last_launch_count()
         del out
+    launches = _native.total_launch_count() - launches0
     torch.cuda.synchronize(dev)
     clocks.mark(t_begin, time.time())
     time.sleep(0.1)

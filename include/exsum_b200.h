@@ -107,6 +107,9 @@ int exsum_release_cache(void);
  * (instrumentation for bench.py's gpu_launches). */
 int exsum_last_launch_count(void);
 
+/* Cumulative number of kernels launched by this library on this thread. */
+long long exsum_total_launch_count(void);
+
 /* Per-kernel CUDA-event profiling of the calls made on this thread (for
  * bench.py's roofline): enable (clears old records), run, synchronize, then
  * read each launch's name, algorithmic bytes (compulsory reads + writes) and

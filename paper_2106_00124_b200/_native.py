@@ -32,6 +32,7 @@ EXPORTS = (
     "exsum_run_host",
     "exsum_release_cache",
     "exsum_last_launch_count",
+    "exsum_total_launch_count",
     "exsum_profile_enable",
     "exsum_profile_count",
     "exsum_profile_get",
@@ -63,6 +64,7 @@ def load():
         L.exsum_abi_version.restype = ci
         L.exsum_last_error.restype = ctypes.c_char_p
         L.exsum_last_launch_count.restype = ci
+        L.exsum_total_launch_count.restype = ctypes.c_longlong
         L.exsum_workspace_bytes.argtypes = [ci, ci, ci, ci, i64p, i64p, ctypes.POINTER(sz)]
         L.exsum_workspace_bytes.restype = ci
         for name in ("exsum_bdbs_included", "exsum_bdbsc_excluded", "exsum_box_complement_excluded"):
@@ -135,6 +137,10 @@ def profile_records():
         check(L.exsum_profile_get(i, buf, 64, ctypes.byref(b), ctypes.byref(ms)))
         out.append((buf.value.decode(), float(b.value), float(ms.value)))
     return out
+
+
+def total_launch_count() -> int:
+    return int(load().exsum_total_launch_count())
 
 
 def last_launch_count() -> int:

@@ -389,6 +389,7 @@ int validate(int route, int dtype, int op, int d, const int64_t* ext, const int6
 }
 
 thread_local int g_last_launches = 0;
+thread_local long long g_total_launches = 0;
 
 int run_device(int route, const void* in, void* out, int dtype, int op, int d, const int64_t* ext,
                const int64_t* box, void* ws, size_t ws_bytes, void* stream) {
@@ -537,6 +538,7 @@ int run_stage_device(int stage, int dtype, int op, int d, const int64_t* ext, co
                  (cudaStream_t)stream, &launches);
   if (rc) return rc;
   g_last_launches = launches;
+  g_total_launches += launches;
   return cuda_check("kernel launch");
 }
 
@@ -581,6 +583,8 @@ int exsum_abi_version(void) { return EXSUM_ABI_VERSION; }
 const char* exsum_last_error(void) { return g_err.c_str(); }
 
 int exsum_last_launch_count(void) { return g_last_launches; }
+
+long long exsum_total_launch_count(void) { return g_total_launches; }
 
 int exsum_workspace_bytes(int route, int dtype, int op, int d, const int64_t* ext,
                           const int64_t* box, size_t* bytes) {
@@ -634,6 +638,7 @@ int exsum_windowed_pass(const void* in, void* out, int dtype, int op, int d, con
     rc = launch_pass(dtype, op, in, out, prod(ext, 0, axis), n, prod(ext, axis + 1, d), k, nullptr, st);
     if (rc < 0) return fail(EXSUM_ECONFIG, "no kernel for this dtype/operator");
     g_last_launches = rc;
+    g_total_launches += rc;
   }
   return cuda_check("kernel launch");
 }

@@ -101,7 +101,7 @@ k_fused_pair(const T* __restrict__ in, T* __restrict__ out, int64_t outer, int64
     issue(u0);
     issue(u0 + 1);
     cp_async_wait<1>();
-    CT cur[U];  // raw rows of the current unit
+    CT cur[U];  // raw rows of the current unit (block j's rows become S in turn)
     int len = rows_of(u0);
 #pragma unroll
     for (int r = 0; r < U; ++r)
@@ -122,8 +122,23 @@ k_fused_pair(const T* __restrict__ in, T* __restrict__ out, int64_t outer, int64
           tails[i] = (Tail && rr < rows_u) ? Tail[o * n1 + us + rr] : ident;
         }
       }
-      if (us + rows_u < n1) cp_async_wait<1>();  // unit u+1 (its first block) has landed
+      // the next unit's rows, all at once into registers; the stitch of the
+      // last block reads them there.  ROW_WIN keeps the whole next unit in
+      // registers across the row op (its slot is refilled right away);
+      // ROW_EXCL's row op needs those registers, so it keeps only the stitch
+      // rows and reloads the unit after the row op.
+      constexpr bool EARLY = true;
+      constexpr int NX = EARLY ? U : K1;
+      const int nlen_u = rows_of(u + 1);
       const T* sn = raw + ((u + 1 - u0) & 1) * (U * N2) + col;
+      CT nxt[NX];
+      if (nlen_u > 0) {
+        cp_async_wait<1>();  // unit u+1 has landed (u+2 may still be in flight)
+#pragma unroll
+        for (int r = 0; r < NX; ++r)
+          if (r < nlen_u) nxt[r] = *reinterpret_cast<const CT*>(sn + r * N2);
+      }
+      if constexpr (EARLY) issue(u + 3);  // refills the slot unit u+1 just vacated
 #pragma unroll
       for (int jb = 0; jb < G; ++jb) {
         const int64_t bs = us + (int64_t)jb * K1;
@@ -147,24 +162,14 @@ k_fused_pair(const T* __restrict__ in, T* __restrict__ out, int64_t outer, int64
             const int nlen = (int)(nrows < K1 ? nrows : K1);
             *reinterpret_cast<CT*>(wst + (jb * K1) * ROWP + pcol) = cur[jb * K1];
             const int nb0 = jb + 1 < G ? (jb + 1) * K1 : 0;  // in range for the dead branch
-            CT P;
-            if (jb + 1 < G) {
-              P = cur[nb0];
-            } else {
-              P = *reinterpret_cast<const CT*>(sn);
-            }
+            CT P = jb + 1 < G ? cur[nb0] : nxt[0];
 #pragma unroll
             for (int r = 1; r < K1; ++r) {
               const int jj = r - 1;
               if (jj >= 1 && jj < nlen) {
-                CT a;
-                if (jb + 1 < G) {
-                  a = cur[nb0 + jj];
-                } else {
-                  a = *reinterpret_cast<const CT*>(sn + jj * N2);
-                }
+                const CT av = jb + 1 < G ? cur[nb0 + jj] : nxt[jj];
 #pragma unroll
-                for (int j = 0; j < TV; ++j) P.v[j] = Op::apply(P.v[j], a.v[j]);
+                for (int j = 0; j < TV; ++j) P.v[j] = Op::apply(P.v[j], av.v[j]);
               }
               CT w;
 #pragma unroll
@@ -174,18 +179,19 @@ k_fused_pair(const T* __restrict__ in, T* __restrict__ out, int64_t outer, int64
           }
         }
       }
-      // next unit's raw rows into registers; its slot is then free to refill
-      len = rows_of(u + 1);
-      if (u + 1 < u_end) {
+      len = nlen_u;
+      if constexpr (EARLY) {
+        if (u + 1 < u_end) {
 #pragma unroll
-        for (int r = 0; r < U; ++r)
-          if (r < len) cur[r] = *reinterpret_cast<const CT*>(sn + r * N2);
+          for (int r = 0; r < U; ++r) cur[r] = nxt[r];
+        }
       }
-      issue(u + 3);
       __syncthreads();
 
       // ---- row operation on the rows_u rows of the stage (warp per row) ----
-#pragma unroll
+      // ROW_EXCL: one row at a time (two interleaved rows exceed 255
+      // registers); ROW_WIN: unrolled, rows interleave for ILP
+#pragma unroll (MODE == ROW_EXCL ? 1 : RPW)
       for (int ri = 0; ri < RPW; ++ri) {
         const int rr = warp + ri * NW;
         if (rr >= rows_u) break;
@@ -242,10 +248,21 @@ k_fused_pair(const T* __restrict__ in, T* __restrict__ out, int64_t outer, int64
             *reinterpret_cast<VT*>(mine + v * VE) = q;
           }
         } else {
-          // full-row prefix / suffix: lane fold, warp scans, S in place
-          T lt = a[0];
+          // full-row prefix / suffix.  The lane chunk is cut into SUB
+          // sub-chunks whose folds and scans run as independent chains
+          // (latency ~C/SUB + log2(32) steps instead of ~3C).
+          constexpr int SUB = C >= 16 ? 4 : (C >= 8 ? 2 : 1);
+          constexpr int CS = C / SUB;
+          T st[SUB];
 #pragma unroll
-          for (int j = 1; j < C; ++j) lt = Op::apply(lt, a[j]);
+          for (int q = 0; q < SUB; ++q) st[q] = a[q * CS];
+#pragma unroll
+          for (int j = 1; j < CS; ++j)
+#pragma unroll
+            for (int q = 0; q < SUB; ++q) st[q] = Op::apply(st[q], a[q * CS + j]);
+          T lt = st[0];
+#pragma unroll
+          for (int q = 1; q < SUB; ++q) lt = Op::apply(lt, st[q]);
           T pin = lt, sin = lt;
 #pragma unroll
           for (int d = 1; d < 32; d <<= 1) {
@@ -258,22 +275,45 @@ k_fused_pair(const T* __restrict__ in, T* __restrict__ out, int64_t outer, int64
           T suf = __shfl_down_sync(0xffffffffu, sin, 1);
           if (lane == 0) pre = ident;
           if (lane == 31) suf = ident;
+          // per sub-chunk carries: S enters from the right, P from the left
+          T sc[SUB], pc[SUB];
+          sc[SUB - 1] = suf;
+#pragma unroll
+          for (int q = SUB - 2; q >= 0; --q) sc[q] = Op::apply(st[q + 1], sc[q + 1]);
+          pc[0] = pre;
+#pragma unroll
+          for (int q = 1; q < SUB; ++q) pc[q] = Op::apply(pc[q - 1], st[q - 1]);
           {
-            T run = suf;
+            // S chains per sub-chunk, written back as 16-byte vectors (a
+            // scalar store at the 36-word lane stride would be 4-way conflicted)
+            static_assert(CS % VE == 0, "sub-chunks hold whole vectors");
+            T run[SUB];
 #pragma unroll
-            for (int v = CV - 1; v >= 0; --v) {
-              VT q;
+            for (int q = 0; q < SUB; ++q) run[q] = sc[q];
 #pragma unroll
-              for (int j = VE - 1; j >= 0; --j) {
-                run = Op::apply(a[v * VE + j], run);
-                q.v[j] = run;
-              }
-              *reinterpret_cast<VT*>(mine + v * VE) = q;
+            for (int jv = CS / VE - 1; jv >= 0; --jv) {
+              VT tq[SUB];
+#pragma unroll
+              for (int j = VE - 1; j >= 0; --j)
+#pragma unroll
+                for (int q = 0; q < SUB; ++q) {
+                  run[q] = Op::apply(a[q * CS + jv * VE + j], run[q]);
+                  tq[q].v[j] = run[q];
+                }
+#pragma unroll
+              for (int q = 0; q < SUB; ++q)
+                *reinterpret_cast<VT*>(mine + q * CS + jv * VE) = tq[q];
             }
           }
           __syncwarp();
-          const T tail = tails[ri];
-          T pe = pre;
+          T tail = tails[0];
+#pragma unroll
+          for (int i = 1; i < RPW; ++i)
+            if (ri == i) tail = tails[i];
+          // out[x] = P[x-1] (+) S[x+k] (+) tail; P runs per sub-chunk from pc[q]
+          T pe[SUB];
+#pragma unroll
+          for (int q = 0; q < SUB; ++q) pe[q] = pc[q];
           if (kvec) {
             // the shift keeps vector alignment: S[x+k] read as 16-byte vectors
 #pragma unroll
@@ -288,19 +328,22 @@ k_fused_pair(const T* __restrict__ in, T* __restrict__ out, int64_t outer, int64
               }
 #pragma unroll
               for (int j = 0; j < VE; ++j) {
-                const T ov = Op::apply(Op::apply(pe, sq.v[j]), tail);
-                pe = Op::apply(pe, a[v * VE + j]);
-                a[v * VE + j] = ov;
+                const int e = v * VE + j;
+                const int q = e / CS;
+                const T ov = Op::apply(Op::apply(pe[q], sq.v[j]), tail);
+                pe[q] = Op::apply(pe[q], a[e]);
+                a[e] = ov;
               }
             }
           } else {
 #pragma unroll
-            for (int j = 0; j < C; ++j) {
-              const int64_t y = (int64_t)lane * C + j + kx;
+            for (int e = 0; e < C; ++e) {
+              const int q = e / CS;
+              const int64_t y = (int64_t)lane * C + e + kx;
               const T sv = y < N2 ? wrow[(y / C) * CH + (y % C)] : ident;
-              const T ov = Op::apply(Op::apply(pe, sv), tail);
-              pe = Op::apply(pe, a[j]);
-              a[j] = ov;
+              const T ov = Op::apply(Op::apply(pe[q], sv), tail);
+              pe[q] = Op::apply(pe[q], a[e]);
+              a[e] = ov;
             }
           }
           __syncwarp();
@@ -317,6 +360,14 @@ k_fused_pair(const T* __restrict__ in, T* __restrict__ out, int64_t outer, int64
       __syncthreads();
       for (int r = 0; r < rows_u; ++r)
         st_stream<T, TV>(dst + (us + r) * N2, *reinterpret_cast<const CT*>(wst + r * ROWP + pcol));
+      if constexpr (!EARLY) {
+        if (u + 1 < u_end) {
+#pragma unroll
+          for (int r = 0; r < U; ++r)
+            if (r < nlen_u) cur[r] = *reinterpret_cast<const CT*>(sn + r * N2);
+        }
+        issue(u + 3);  // refills the slot unit u+1 just vacated
+      }
     }
     cp_async_wait<0>();
   }

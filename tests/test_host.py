@@ -15,7 +15,7 @@ ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 
 def _header_functions():
     text = open(os.path.join(ROOT, "include", "exsum_b200.h")).read()
-    return re.findall(r"^\s*(?:const\s+)?\w+\s*\*?\s*(exsum_\w+)\s*\(", text, re.M)
+    return re.findall(r"^\s*(?:const\s+)?(?:long\s+)?\w+\s*\*?\s*(exsum_\w+)\s*\(", text, re.M)
 
 
 def test_library_exports_every_header_symbol():
