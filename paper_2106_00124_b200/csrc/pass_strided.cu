@@ -320,11 +320,12 @@ int go_reg(const T* in, T* out, int64_t outer, int64_t n, int64_t inner, int k,
   const int64_t want_threads = (int64_t)num_sms() * 1536;
   int64_t nseg = (want_threads + lines - 1) / lines;
   const int64_t nblocks = (nout + k - 1) / k;
-  // halo cost is one block per segment: keep >= 16 blocks per segment for
-  // arrays that stream from HBM, but go down to 2 for L2-resident ones (there
-  // the kernel is latency bound and parallelism wins)
+  // halo cost is one block per segment (re-read, mostly from L2 since the
+  // neighbouring segment streams it at the same time): split only as far as
+  // occupancy needs, down to 4 blocks per segment (2 for L2-resident arrays,
+  // where the kernel is latency bound)
   const bool small = outer * n * inner * (int64_t)sizeof(T) < ((int64_t)64 << 20);
-  int64_t max_seg = nblocks / (small ? 2 : 16);
+  int64_t max_seg = nblocks / (small ? 2 : 4);
   if (max_seg < 1) max_seg = 1;
   if (nseg > max_seg) nseg = max_seg;
   if (nseg < 1) nseg = 1;
