@@ -410,6 +410,7 @@ int run_device(int route, const void* in, void* out, int dtype, int op, int d, c
   rc = dispatch(route, s, dtype, op, in, out, ar, (cudaStream_t)stream, &launches);
   if (rc) return rc;
   g_last_launches = launches;
+  g_total_launches += launches;
   return cuda_check("kernel launch");
 }
 
