@@ -110,7 +110,7 @@ class CudaEngine:
     def _stream(self):
         return self.torch.cuda.current_stream(self.device).cuda_stream
 
-    def axis0(self, x_ext, n_out, box, extra_kind, out=None):
+    def axis0(self, x_ext, n_out, box, extra_kind, out=None, extra=None):
         torch = self.torch
         ext_in = tuple(int(v) for v in x_ext.shape)
         dt, op = _native.DTYPE[self.dtype_name], _native.OP[self.op]
@@ -118,8 +118,9 @@ class CudaEngine:
         ws = self._workspace(nbytes)
         if out is None:
             out = torch.empty((n_out,) + ext_in[1:], dtype=x_ext.dtype, device=self.device)
-        extra = None
-        if extra_kind == 1:
+        if extra is not None:
+            pass
+        elif extra_kind == 1:
             extra = torch.empty((n_out,) + ext_in[1:-1], dtype=x_ext.dtype, device=self.device)
         elif extra_kind == 2:
             extra = torch.empty(1, dtype=torch.int64 if self.dtype_name == "int64" else torch.float64,
@@ -189,8 +190,14 @@ class DistComm:
         self.nccl = dist.get_backend() == "nccl"
 
     def exchange_halo(self, plan, x_ext, n_own):
-        """Send my first halo(r-1) planes to the rank whose halo I hold; receive
-        halo(r) planes into x_ext[n_own:]."""
+        """Blocking form of start_halo()."""
+        for req in self.start_halo(plan, x_ext, n_own):
+            req.wait()
+
+    def start_halo(self, plan, x_ext, n_own):
+        """Post the halo exchange (send my first halo(r-1) planes to the rank
+        whose halo I hold; receive halo(r) planes into x_ext[n_own:]) and
+        return the requests; wait() on them before reading the halo."""
         dist = self.dist
         ops = []
         r = self.rank
@@ -210,15 +217,11 @@ class DistComm:
             src = plan.source_of_halo(r)
             recv = x_ext[n_own:n_own + h]
             ops.append(dist.P2POp(dist.irecv, recv, src))
-        if ops:
-            if self.nccl:
-                for req in dist.batch_isend_irecv(ops):
-                    req.wait()
-            else:
-                reqs = [(dist.isend if o.op is dist.isend else dist.irecv)(o.tensor, o.peer)
-                        for o in ops]
-                for req in reqs:
-                    req.wait()
+        if not ops:
+            return []
+        if self.nccl:
+            return list(dist.batch_isend_irecv(ops))
+        return [(dist.isend if o.op is dist.isend else dist.irecv)(o.tensor, o.peer) for o in ops]
 
     def all_gather_rows(self, t, counts):
         """Concatenate per-rank tensors of `counts[q]` rows along axis 0."""
@@ -288,8 +291,10 @@ class ShardedRunner:
     def __call__(self, x_ext):
         if tuple(x_ext.shape) != self.local_shape():
             raise UsageError(f"slab shape {tuple(x_ext.shape)} != {self.local_shape()}")
-        self.comm.exchange_halo(self.plan, x_ext, self.n_own)
-        return self.finish(x_ext)
+        reqs = self.comm.start_halo(self.plan, x_ext, self.n_own)
+        y, extra = self.stage1(x_ext, reqs)
+        combined = self.combine(extra, x_ext.device)
+        return self.stage2(y, combined)
 
     def finish(self, x_ext):
         """Stage 1, the combine step and stage 2 (after the halo is in place)."""
@@ -299,11 +304,38 @@ class ShardedRunner:
 
     # -- phases (also driven one virtual rank at a time by run_loopback) --------
 
-    def stage1(self, x_ext):
+    def stage1(self, x_ext, halo_reqs=None):
+        """Axis-0 pass of the own planes.  With a halo in flight, the blocks
+        that do not need it run first (a standalone pass over the own planes
+        is exact for every block but the last, whose stitch partner is the
+        halo), then the last block once the halo has landed."""
         extra_kind = {"bdbs": 0, "bdbsc": 2, "box-complement": 1}[self.route]
         if self.n_own == 0:
+            for req in halo_reqs or []:
+                req.wait()
             return None, None
-        return self.engine.axis0(x_ext, self.n_own, self.k, extra_kind)
+        k0 = self.k[0]
+        split = bool(halo_reqs) and self.halo > 0 and self.n_own >= 2 * k0 and k0 > 1
+        if not split:
+            for req in halo_reqs or []:
+                req.wait()
+            return self.engine.axis0(x_ext, self.n_own, self.k, extra_kind)
+        import torch
+
+        head = self.n_own - k0
+        y = torch.empty((self.n_own,) + self.ext[1:], dtype=x_ext.dtype, device=x_ext.device)
+        extra = None
+        if extra_kind == 1:
+            extra = torch.empty((self.n_own,) + self.ext[1:-1], dtype=x_ext.dtype, device=x_ext.device)
+        _, e_a = self.engine.axis0(x_ext[:self.n_own], head, self.k, extra_kind, out=y[:head],
+                                   extra=None if extra is None else extra[:head])
+        for req in halo_reqs:
+            req.wait()
+        _, e_b = self.engine.axis0(x_ext[head:], k0, self.k, extra_kind, out=y[head:],
+                                   extra=None if extra is None else extra[head:])
+        if extra_kind == 2:
+            extra = e_a + e_b
+        return y, extra
 
     def local_extra(self, extra, device):
         import torch
@@ -317,7 +349,11 @@ class ShardedRunner:
     def combine(self, extra, device):
         extra = self.local_extra(extra, device)
         if self.route == "bdbsc":
-            return combine_totals(self.comm.all_gather_scalars(extra), self.is_int)
+            # stays on the device (no host sync in the step): a fixed-order
+            # reduction of the world's partial totals
+            import torch
+
+            return torch.stack(self.comm.all_gather_scalars(extra)).sum(dim=0)
         if self.route == "box-complement":
             counts = [self.plan.bounds(q)[1] - self.plan.bounds(q)[0] for q in range(self.world)]
             R = self.comm.all_gather_rows(extra, counts)
@@ -330,11 +366,7 @@ class ShardedRunner:
         if self.route == "bdbs":
             return self.engine.bdbs_finish(y, self.k, None)
         if self.route == "bdbsc":
-            import torch
-
-            tdev = torch.tensor([combined], dtype=torch.int64 if self.is_int else torch.float64,
-                                device=y.device)
-            return self.engine.bdbs_finish(y, self.k, tdev)
+            return self.engine.bdbs_finish(y, self.k, combined.reshape(1).contiguous())
         return self.engine.bc_finish(y, self.k, combined[self.start:self.end])
 
 
@@ -362,7 +394,12 @@ class _LoopbackComm:
         return torch.cat([e[:c] for e, c in zip(self.extras, counts)], dim=0)
 
 
-def run_loopback(route, ops, a, box, world, engine):
+class _Done:
+    def wait(self):
+        return None
+
+
+def run_loopback(route, ops, a, box, world, engine, split=True):
     """Run the sharded route with `world` virtual ranks in this process (one
     GPU): halos are sliced from the global array, the combine step sees every
     rank's stage-1 output.  Returns the concatenated output.  This exercises
@@ -376,7 +413,8 @@ def run_loopback(route, ops, a, box, world, engine):
     ys, extras = [], []
     for r in runners:
         x_ext = a[r.start:r.end + r.halo]
-        y, e = r.stage1(x_ext.contiguous())
+        # split=True takes the overlap path (interior blocks, then the last one)
+        y, e = r.stage1(x_ext.contiguous(), [_Done()] if split and r.halo > 0 else None)
         ys.append(y)
         extras.append(r.local_extra(e, a.device))
     comm.extras = extras

@@ -16,8 +16,9 @@ class OracleEngine:
         self.op = op
         self.dtype_name = dtype_name
 
-    def axis0(self, x_ext, n_out, box, extra_kind):
-        a = x_ext.numpy()
+    def axis0(self, x_ext, n_out, box, extra_kind, out=None, extra=None):
+        extra_out = extra
+        a = x_ext.contiguous().numpy()
         y = orc.windowed_pass(a, 0, min(box[0], a.shape[0]), self.op)[:n_out]
         extra = None
         own = a[:n_out]
@@ -30,7 +31,14 @@ class OracleEngine:
                     extra = torch.tensor([int(own.sum(dtype=np.int64))], dtype=torch.int64)
             else:
                 extra = torch.tensor([float(own.astype(np.float64).sum())], dtype=torch.float64)
-        return torch.from_numpy(np.ascontiguousarray(y)), extra
+        y = torch.from_numpy(np.ascontiguousarray(y))
+        if out is not None:  # write into the caller's views, like the CUDA engine
+            out.copy_(y)
+            y = out
+        if extra_out is not None and extra is not None and extra_kind == 1:
+            extra_out.copy_(extra)
+            extra = extra_out
+        return y, extra
 
     def bdbs_finish(self, y, box, total):
         a = y.numpy()

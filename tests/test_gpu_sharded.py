@@ -46,7 +46,10 @@ def test_loopback_matches_single_gpu(ext, box, mono, world):
               "box-complement": ex.box_complement_excluded}[route]
         single = fn(ex.Tensor(ops, x), box).data.cpu().numpy()
         sharded = run_loopback(route, ops, x, box, world, engine).cpu().numpy()
+        plain = run_loopback(route, ops, x, box, world, engine, split=False).cpu().numpy()
         assert sharded.shape == single.shape
+        if route != "bdbsc":  # the split only regroups the per-rank total
+            assert np.array_equal(sharded.view(np.uint8), plain.view(np.uint8)), route
         if route != "bdbs" and ops.dtype.kind == "f":
             # reassociated float totals / row reductions: the parity contract
             k = tuple(min(b, n) for b, n in zip(box, ext))
