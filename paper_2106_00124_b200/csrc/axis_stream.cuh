@@ -1,0 +1,211 @@
+// axis_stream.cuh -- strided windowed pass through a cp.async shared ring.
+//
+// Same algorithm and association as windowed_sum_axis (reference
+// pkg/src/exsum/scan.py:61-102) on a view [outer, n, inner]: in-block
+// right-nested suffix, left-nested prefix of the next block, one stitch
+// combine.  The B200 mapping is the streaming half of fused_pair.cuh: a CTA
+// owns a strip of N2 = 32*C consecutive columns of one outer index and a
+// segment of the axis; every thread owns one 16-byte column vector and
+// prefetches its own vectors of units u+2, u+3 (U = 16 rows) with cp.async
+// into a 2-slot ring, the suffix/prefix run in registers, results go straight
+// to HBM as coalesced 16-byte stores.
+//
+// Piggy-backed reductions of the raw input (the pass reads it anyway):
+//   EX == 1: R, the fold of every row of the last axis (box-complement,
+//            exsum_capi.cu): the rows of a unit are in shared memory once it
+//            lands, so warps fold them there (lane chunk + warp shuffle) and
+//            write one partial per (row, strip) -- no register butterfly;
+//   EX == 2: the BDBSC total, folded per thread from registers.
+#pragma once
+
+#include "exsum_common.cuh"
+#include "exsum_launch.h"
+
+namespace exsum {
+
+template <class T, class Op, int C, int K1, int EX>
+__global__ void __launch_bounds__(32 * C / (16 / sizeof(T)), 1)
+k_axis_stream(const T* __restrict__ in, T* __restrict__ out, int64_t outer, int64_t n1,
+              int64_t inner, int64_t nout, int64_t seg_len, int64_t nseg,
+              const typename AccOf<T>::type* __restrict__ total, T* __restrict__ rowpart,
+              int64_t row_len, typename AccOf<T>::type* __restrict__ tpart) {
+  typedef typename AccOf<T>::type Acc;
+  constexpr int VE = 16 / sizeof(T);
+  constexpr int N2 = 32 * C;                     // strip width (columns)
+  constexpr int NT = N2 / VE;                    // threads
+  constexpr int NW = NT / 32;
+  constexpr int G = 16 / K1 > 0 ? 16 / K1 : 1;   // blocks per unit
+  constexpr int U = G * K1;                      // rows per unit
+  constexpr int CV = C / VE;                     // vectors per lane chunk of a row
+  typedef Vec<T, VE> VT;
+  extern __shared__ __align__(16) unsigned char smem[];
+  T* raw = reinterpret_cast<T*>(smem);  // [2][U][N2]
+  const int tid = threadIdx.x;
+  const int lane = tid & 31;
+  const int warp = tid >> 5;
+  const int col = tid * VE;
+  const T tot = total ? (T)(*total) : T(0);
+  const bool epi = total != nullptr;
+  const int64_t last_bs = (int64_t)K1 * ((n1 - 1) / K1);
+  const int64_t strips = inner / N2;
+  const int64_t items = outer * strips * nseg;
+  const int64_t rows_total = outer * nout * (inner / row_len);  // rows of the last axis
+  const int64_t parts = EX == 1 ? row_len / N2 : 0;              // strips per row
+  Acc tacc[VE];
+#pragma unroll
+  for (int j = 0; j < VE; ++j) tacc[j] = Op::template identity<Acc>();
+
+  for (int64_t item = blockIdx.x; item < items; item += gridDim.x) {
+    const int64_t strip = item % strips;
+    const int64_t rest = item / strips;
+    const int64_t o = rest % outer;
+    const int64_t seg = rest / outer;
+    const int64_t xs = seg * seg_len;  // multiple of U
+    const int64_t xe = xs + seg_len < nout ? xs + seg_len : nout;
+    const int64_t u0 = xs / U;
+    const int64_t u_end = (xe + U - 1) / U;
+    const T* src = in + o * n1 * inner + strip * N2 + col;
+    T* dst = out + o * nout * inner + strip * N2 + col;
+
+    auto rows_of = [&](int64_t ui) -> int {
+      const int64_t avail = n1 - ui * U;
+      const int64_t want = ui >= u_end ? K1 - 1 : U;
+      return (int)(avail < want ? (avail > 0 ? avail : 0) : want);
+    };
+    auto issue = [&](int64_t ui) {
+      const int rows = rows_of(ui);
+      T* d = raw + ((ui - u0) & 1) * (U * N2) + col;
+      for (int r = 0; r < rows; ++r) cp_async16(d + r * N2, src + (ui * U + r) * inner);
+      cp_async_commit();
+    };
+    // EX == 1: fold the own rows of unit ui from its slot (all columns landed)
+    auto fold_rows = [&](int64_t ui, const T* slot, int nrows) {
+      if constexpr (EX == 1) {
+        __syncthreads();  // every thread's copies of this unit are visible
+        const int64_t inseg = xe - ui * U;
+        const int own = (int)(nrows < inseg ? nrows : inseg);
+        for (int rr = warp; rr < own; rr += NW) {
+          const T* row = slot + rr * N2 + lane * C;
+          T acc = Op::template identity<T>();
+#pragma unroll
+          for (int v = 0; v < CV; ++v) {
+            const VT q = *reinterpret_cast<const VT*>(row + v * VE);
+#pragma unroll
+            for (int j = 0; j < VE; ++j) acc = Op::apply(acc, q.v[j]);
+          }
+#pragma unroll
+          for (int d = 16; d >= 1; d >>= 1) acc = Op::apply(acc, __shfl_xor_sync(0xffffffffu, acc, d));
+          if (lane == 0) {
+            const int64_t e = (o * nout + ui * U + rr) * inner + strip * N2;  // first element
+            rowpart[((e % row_len) / N2) * rows_total + e / row_len] = acc;
+          }
+        }
+        __syncthreads();  // readers done before the slot is refilled
+      }
+    };
+
+    issue(u0);
+    issue(u0 + 1);
+    cp_async_wait<1>();
+    VT cur[U];
+    int len = rows_of(u0);
+    fold_rows(u0, raw, len);
+#pragma unroll
+    for (int r = 0; r < U; ++r)
+      if (r < len) cur[r] = *reinterpret_cast<const VT*>(raw + col + r * N2);
+    issue(u0 + 2);
+
+    for (int64_t u = u0; u < u_end; ++u) {
+      const int64_t us = u * U;
+      const int rows_u = len;
+      if constexpr (EX == 2) {
+#pragma unroll
+        for (int r = 0; r < U; ++r)
+          if (r < rows_u && us + r < xe) {
+#pragma unroll
+            for (int j = 0; j < VE; ++j) tacc[j] = Op::apply(tacc[j], (Acc)cur[r].v[j]);
+          }
+      }
+      const int nlen_u = rows_of(u + 1);
+      const T* sn = raw + ((u + 1 - u0) & 1) * (U * N2) + col;
+      VT nxt[U];
+      if (nlen_u > 0) {
+        cp_async_wait<1>();  // unit u+1 has landed (u+2 may still be in flight)
+        if (u + 1 < u_end) fold_rows(u + 1, sn - col, nlen_u);
+#pragma unroll
+        for (int r = 0; r < U; ++r)
+          if (r < nlen_u) nxt[r] = *reinterpret_cast<const VT*>(sn + r * N2);
+      }
+      issue(u + 3);
+#pragma unroll
+      for (int jb = 0; jb < G; ++jb) {
+        const int64_t bs = us + (int64_t)jb * K1;
+        if (jb * K1 < rows_u && bs < xe) {  // the unit may reach into a shard's halo
+          const int blen = (int)(n1 - bs < K1 ? n1 - bs : K1);
+#pragma unroll
+          for (int r = K1 - 2; r >= 0; --r)
+            if (r < blen - 1) {
+#pragma unroll
+              for (int j = 0; j < VE; ++j)
+                cur[jb * K1 + r].v[j] = Op::apply(cur[jb * K1 + r].v[j], cur[jb * K1 + r + 1].v[j]);
+            }
+          auto put = [&](int r, VT w) {
+            if (epi) {
+#pragma unroll
+              for (int j = 0; j < VE; ++j) w.v[j] = OpAdd::inverse<T>(tot, w.v[j]);
+            }
+            st_stream<T, VE>(dst + (bs + r) * inner, w);
+          };
+          if (bs == last_bs) {
+#pragma unroll
+            for (int r = 0; r < K1; ++r)
+              if (r < blen) put(r, cur[jb * K1 + r]);
+          } else {
+            const int64_t nrows = n1 - bs - K1;
+            const int nlen = (int)(nrows < K1 ? nrows : K1);
+            put(0, cur[jb * K1]);
+            const int nb0 = jb + 1 < G ? (jb + 1) * K1 : 0;
+            VT P = jb + 1 < G ? cur[nb0] : nxt[0];
+#pragma unroll
+            for (int r = 1; r < K1; ++r) {
+              const int jj = r - 1;
+              if (jj >= 1 && jj < nlen) {
+                const VT av = jb + 1 < G ? cur[nb0 + jj] : nxt[jj];
+#pragma unroll
+                for (int j = 0; j < VE; ++j) P.v[j] = Op::apply(P.v[j], av.v[j]);
+              }
+              VT w;
+#pragma unroll
+              for (int j = 0; j < VE; ++j) w.v[j] = Op::apply(cur[jb * K1 + r].v[j], P.v[j]);
+              put(r, w);
+            }
+          }
+        }
+      }
+      len = nlen_u;
+      if (u + 1 < u_end) {
+#pragma unroll
+        for (int r = 0; r < U; ++r) cur[r] = nxt[r];
+      }
+    }
+    cp_async_wait<0>();
+    __syncthreads();  // the next item refills both slots
+  }
+  if constexpr (EX == 2) {
+    __shared__ Acc sh[NW];
+    Acc ta = tacc[0];
+#pragma unroll
+    for (int j = 1; j < VE; ++j) ta = Op::apply(ta, tacc[j]);
+#pragma unroll
+    for (int d = 16; d >= 1; d >>= 1) ta = Op::apply(ta, __shfl_xor_sync(0xffffffffu, ta, d));
+    if (lane == 0) sh[warp] = ta;
+    __syncthreads();
+    if (tid == 0) {
+      Acc t = sh[0];
+      for (int w = 1; w < NW; ++w) t = Op::apply(t, sh[w]);
+      tpart[blockIdx.x] = t;
+    }
+  }
+}
+
+}  // namespace exsum

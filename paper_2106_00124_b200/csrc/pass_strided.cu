@@ -444,6 +444,27 @@ int launch_rows_pass(int dtype, int op, const void* in, void* out, int64_t rows,
 
 int launch_strided_bulk(int dtype, int op, const void* in, void* out, int64_t outer, int64_t n,
                         int64_t inner, int64_t k, const void* total, cudaStream_t s);
+int launch_axis_stream_f32(const void*, void*, int64_t, int64_t, int64_t, int64_t, const void*,
+                           cudaStream_t, PassExtra*);
+int launch_axis_stream_f64(const void*, void*, int64_t, int64_t, int64_t, int64_t, const void*,
+                           cudaStream_t, PassExtra*);
+int launch_axis_stream_i64add(const void*, void*, int64_t, int64_t, int64_t, int64_t, const void*,
+                              cudaStream_t, PassExtra*);
+int launch_axis_stream_i64max(const void*, void*, int64_t, int64_t, int64_t, int64_t, const void*,
+                              cudaStream_t, PassExtra*);
+
+// EXSUM_AXIS_STREAM=0|1|2 (measurements): never / every eligible pass except
+// those folding row partials (default; the register butterfly of
+// k_strided_reg is faster there: the shared-memory fold needs two CTA
+// barriers per unit) / every eligible pass
+static int axis_stream_mode() {
+  static int mode = -1;
+  if (mode < 0) {
+    const char* e = getenv("EXSUM_AXIS_STREAM");
+    mode = e ? atoi(e) : 1;
+  }
+  return mode;
+}
 
 // EXSUM_STRIDED=auto|reg|bulk|blockreg|blocks picks the strided kernel (for
 // measurements); auto: register streaming while the register tile fits,
@@ -475,6 +496,15 @@ int launch_pass(int dtype, int op, const void* in, void* out, int64_t outer, int
   if (inner == 1) return launch_rows_pass(dtype, op, in, out, outer, n, k, total, s);
   const int mode = strided_mode();
   const bool big = k > 32 || (dtype != F32 && k > 16);
+  const int am = axis_stream_mode();
+  if (am == 2 || (am == 1 && !(ex && ex->kind == 1))) {
+    int rc = -1;
+    if (dtype == F32 && op == ADD) rc = launch_axis_stream_f32(in, out, outer, n, inner, k, total, s, ex);
+    else if (dtype == F64 && op == ADD) rc = launch_axis_stream_f64(in, out, outer, n, inner, k, total, s, ex);
+    else if (dtype == I64 && op == ADD) rc = launch_axis_stream_i64add(in, out, outer, n, inner, k, total, s, ex);
+    else if (dtype == I64 && op == MAX) rc = launch_axis_stream_i64max(in, out, outer, n, inner, k, total, s, ex);
+    if (rc >= 0) return rc;
+  }
   if (mode == 2 || (mode == 0 && big)) {
     const int rc = launch_strided_bulk(dtype, op, in, out, outer, n, inner, k, total, s);
     if (rc >= 0) return rc;
