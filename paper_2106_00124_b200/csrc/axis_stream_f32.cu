@@ -33,8 +33,7 @@ int go_axis_stream_c(const T* in, T* out, int64_t outer, int64_t n, int64_t inne
   const int64_t cap = (int64_t)num_sms() * per_sm * 4;
   if (EX == 2 && cap > ex->cap) return -1;
   if (grid > cap) grid = cap;
-  cudaFuncSetAttribute(k_axis_stream<T, Op, C, K1, EX>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                       (int)smem);
+  ensure_smem((const void*)k_axis_stream<T, Op, C, K1, EX>, smem);
   k_axis_stream<T, Op, C, K1, EX><<<(unsigned)grid, NT, smem, s>>>(
       in, out, outer, n, inner, nout, seg_len, nseg, total,
       EX == 1 ? (T*)ex->buf : nullptr, EX == 1 ? ex->row_len : N2,
@@ -84,6 +83,7 @@ int go_axis_stream(const T* in, T* out, int64_t outer, int64_t n, int64_t inner,
                    const typename AccOf<T>::type* total, cudaStream_t s, PassExtra* ex) {
   if (((uintptr_t)in % 16) || ((uintptr_t)out % 16)) return -1;
   if (!(k == 2 || k == 4 || k == 8 || k == 16)) return -1;
+  if (n < 64) return -1;  // < 4 units per strip: the ring never fills; register streaming wins
   const int64_t nout = (ex && ex->n_out >= 0) ? ex->n_out : n;
   if (nout != n && outer != 1) return -1;
   if constexpr (sizeof(T) == 4) {

@@ -12,6 +12,10 @@
 #include <cuda_runtime.h>
 #include <stdint.h>
 
+#include <mutex>
+#include <tuple>
+#include <vector>
+
 namespace exsum {
 
 typedef long long i64;
@@ -115,6 +119,21 @@ struct Epilogue {
     return OpAdd::inverse<T>((T)(*total), v);
   }
 };
+
+// Raise a kernel's dynamic shared-memory limit once per (kernel, device, size)
+// instead of on every launch (cudaFuncSetAttribute costs microseconds of host
+// time, which shows on small arrays).
+inline void ensure_smem(const void* fn, size_t bytes) {
+  static std::mutex mu;
+  static std::vector<std::tuple<const void*, int, size_t>> done;
+  int dev = 0;
+  cudaGetDevice(&dev);
+  std::lock_guard<std::mutex> g(mu);
+  for (const auto& t : done)
+    if (std::get<0>(t) == fn && std::get<1>(t) == dev && std::get<2>(t) >= bytes) return;
+  cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)bytes);
+  done.emplace_back(fn, dev, bytes);
+}
 
 // ------------------------------------------- bulk async copies (TMA path) --
 // 1-D cp.async.bulk global->shared with mbarrier completion (sm_90+; SASS

@@ -410,8 +410,7 @@ int go_pair(const T* in, T* out, int64_t outer, int64_t n1, int64_t kx,
   int64_t grid = items;
   const int64_t cap = (int64_t)num_sms() * per_sm * 4;
   if (grid > cap) grid = cap;
-  cudaFuncSetAttribute(k_fused_pair<T, Op, C, K1, MODE, TV>,
-                       cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  ensure_smem((const void*)k_fused_pair<T, Op, C, K1, MODE, TV>, smem);
   k_fused_pair<T, Op, C, K1, MODE, TV><<<(unsigned)grid, NT, smem, s>>>(in, out, outer, n1, kx,
                                                                        seg_len, nseg, total, Tail);
   return 1;

@@ -160,8 +160,7 @@ int go_bulk(const T* in, T* out, int64_t outer, int64_t n, int64_t inner, int64_
   const int64_t cap = (int64_t)num_sms() * 32;
   if (grid > cap) grid = cap;
   if (smem > 48 * 1024)
-    cudaFuncSetAttribute(k_strided_bulk<T, Op>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                         (int)smem);
+    ensure_smem((const void*)k_strided_bulk<T, Op>, smem);
   k_strided_bulk<T, Op><<<(unsigned)grid, 32, smem, s>>>(in, out, outer, n, inner, (int)k,
                                                          seg_len, nseg, R, total);
   return 1;

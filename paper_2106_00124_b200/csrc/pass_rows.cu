@@ -290,8 +290,11 @@ k_rows_tile(const T* __restrict__ in, T* __restrict__ out, int64_t rows, int64_t
   // padded chunk stride, an odd number of 16-byte vectors: 16-byte accesses of
   // 8 consecutive lanes land in 8 distinct bank groups
   const int STRIDE = ((CV + 1) | 1) * VE;
+  // v / CV by multiply-shift: exact for v < 65536 / CV (v <= 33 * CV here)
+  const unsigned cv_magic = (65536u + (unsigned)CV - 1) / (unsigned)CV;
   const int M = C / K;                // blocks per chunk
   static_assert(CMAX % K == 0 && CMAX % VE == 0, "chunk shape");
+  static_assert(CVMAX <= 32, "the multiply-shift division below is exact for CV <= 32");
   typedef Vec<T, VE> VT;
   __shared__ __align__(16) T smem[WARPS][33 * (CMAX + 2 * VE)];
   const int lane = threadIdx.x & 31;
@@ -313,7 +316,8 @@ k_rows_tile(const T* __restrict__ in, T* __restrict__ out, int64_t rows, int64_t
 #pragma unroll 4
     for (int v = lane; v < nload * CV; v += 32) {
       const VT q = ld_stream<T, VE>(reinterpret_cast<const T*>(src + v));
-      *reinterpret_cast<VT*>(sm + (v / CV) * STRIDE + (v % CV) * VE) = q;
+      const int cq = (int)(((unsigned)v * cv_magic) >> 16);  // v / CV (v < 4096)
+      *reinterpret_cast<VT*>(sm + cq * STRIDE + (v - cq * CV) * VE) = q;
     }
     __syncwarp();
     const int64_t c = c0 + lane;
@@ -368,7 +372,8 @@ k_rows_tile(const T* __restrict__ in, T* __restrict__ out, int64_t rows, int64_t
 #pragma unroll 4
     for (int v = lane; v < nstore * CV; v += 32)
       st_stream<T, VE>(reinterpret_cast<T*>(dst + v),
-                       *reinterpret_cast<const VT*>(sm + (v / CV) * STRIDE + (v % CV) * VE));
+                       *reinterpret_cast<const VT*>(sm + (((unsigned)v * cv_magic) >> 16) * STRIDE +
+                                                    (v - (int)(((unsigned)v * cv_magic) >> 16) * CV) * VE));
     __syncwarp();
   }
 }

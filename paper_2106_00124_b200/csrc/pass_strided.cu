@@ -386,8 +386,13 @@ int go_strided(const T* in, T* out, int64_t outer, int64_t n, int64_t inner, int
     const char* e = getenv("EXSUM_VMAX");
     vmax = e ? atoi(e) : 0;
   }
+  static int vextra = -1;  // EXSUM_VEXTRA: vector cap for passes with piggy-backed reductions
+  if (vextra < 0) {
+    const char* e = getenv("EXSUM_VEXTRA");
+    vextra = e ? atoi(e) : 2;
+  }
   int vcap = vmax > 0 ? vmax : 16;
-  if (vmax == 0 && ex && ex->kind != 0 && sizeof(T) == 4 && k > 8) vcap = 2;
+  if (vmax == 0 && ex && ex->kind != 0 && sizeof(T) == 4 && k > 8) vcap = vextra;
   const bool v16 = vcap >= (int)(16 / sizeof(T)) && inner % (16 / sizeof(T)) == 0 && a % 16 == 0;
   const bool v8 = vcap >= 2 && sizeof(T) == 4 && inner % 2 == 0 && a % 8 == 0;  // 8-byte (float2)
   if (strided_mode() == 4 || (k > 32 && strided_mode() != 1)) {

@@ -318,8 +318,7 @@ int go_excl(const T* W, T* out, const T* Tail, int64_t rows, int64_t n, int64_t 
   if (row_bytes <= kExclSmemPerWarpMax) {
     const size_t smem = row_bytes * 4;
     if (smem > 48 * 1024)
-      cudaFuncSetAttribute(k_excl_rows<T, Op, true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                           (int)smem);
+      ensure_smem((const void*)k_excl_rows<T, Op, true>, smem);
     const int64_t cap = (int64_t)num_sms() * 16;
     if (grid > cap) grid = cap;
     k_excl_rows<T, Op, true><<<(unsigned)grid, 128, smem, s>>>(W, out, Tail, rows, n, k, nullptr);
