@@ -15,7 +15,10 @@ import threading
 
 from .errors import ConfigurationError, DeviceError, UsageError
 
-LIB_PATH = os.path.join(os.path.dirname(os.path.abspath(__file__)), "libexsum_b200.so")
+# EXSUM_LIB overrides the library (ablation builds in measurements); the
+# default is the in-tree build.
+LIB_PATH = os.environ.get("EXSUM_LIB") or os.path.join(
+    os.path.dirname(os.path.abspath(__file__)), "libexsum_b200.so")
 
 DTYPE = {"float32": 0, "float64": 1, "int64": 2}
 OP = {"add": 0, "max": 1}

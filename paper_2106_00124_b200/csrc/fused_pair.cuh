@@ -31,6 +31,8 @@
 
 #include <stdlib.h>
 
+#include <type_traits>
+
 #include "exsum_common.cuh"
 #include "exsum_launch.h"
 
@@ -56,7 +58,7 @@ k_fused_pair(const T* __restrict__ in, T* __restrict__ out, int64_t outer, int64
   constexpr int M2 = C / K2;           // row-op blocks per lane chunk
   constexpr int G = 16 / K1 > 0 ? 16 / K1 : 1;  // blocks per unit
   constexpr int U = G * K1;            // rows per unit: register tile, stage, prefetch granule
-  static_assert(C % VE == 0 && (MODE == ROW_EXCL || C % K2 == 0), "shape");
+  static_assert(C % VE == 0 && C % K2 == 0, "shape");
   typedef Vec<T, VE> VT;  // row-op vectors
   typedef Vec<T, TV> CT;  // column vectors of the axis-(d-2) pass
   extern __shared__ __align__(16) unsigned char smem[];
@@ -204,7 +206,22 @@ k_fused_pair(const T* __restrict__ in, T* __restrict__ out, int64_t outer, int64
 #pragma unroll
           for (int j = 0; j < VE; ++j) a[v * VE + j] = q.v[j];
         }
-        if constexpr (MODE == ROW_WIN) {
+        // ROW_EXCL with + and a cubic box: along a row the excluded window sum
+        // is (row total) - (window), so the exact windowed row op plus one
+        // warp reduction replaces the prefix/suffix scans (the float error
+        // scales with the row total, inside the box-complement bound of
+        // tests/parity.py); max has no inverse and keeps the scans below.
+        constexpr bool ADD_EXCL = MODE == ROW_EXCL && std::is_same<Op, OpAdd>::value;
+        if (MODE == ROW_WIN || (ADD_EXCL && kx == K2)) {
+          T rtot = T(0);
+          if constexpr (ADD_EXCL) {
+            T lt = a[0];
+#pragma unroll
+            for (int j = 1; j < C; ++j) lt = Op::apply(lt, a[j]);
+#pragma unroll
+            for (int d = 16; d >= 1; d >>= 1) lt = Op::apply(lt, __shfl_xor_sync(0xffffffffu, lt, d));
+            rtot = lt;
+          }
           // exact in-block scans along the row (blocks of K2 inside the chunk)
           constexpr int NBV = (K2 + VE - 1) / VE;
           VT nbv[NBV];  // neighbour's first block, raw
@@ -237,13 +254,23 @@ k_fused_pair(const T* __restrict__ in, T* __restrict__ out, int64_t outer, int64
             }
           }
           __syncwarp();
+          T etail = T(0);
+          if constexpr (ADD_EXCL) {
+#pragma unroll
+            for (int i = 0; i < RPW; ++i)
+              if (ri == i) etail = tails[i];
+          }
 #pragma unroll
           for (int v = 0; v < CV; ++v) {
             VT q;
 #pragma unroll
             for (int j = 0; j < VE; ++j) {
               const T w = a[v * VE + j];
-              q.v[j] = epi ? OpAdd::inverse<T>(tot, w) : w;
+              if constexpr (ADD_EXCL) {
+                q.v[j] = Op::apply(OpAdd::inverse<T>(rtot, w), etail);
+              } else {
+                q.v[j] = epi ? OpAdd::inverse<T>(tot, w) : w;
+              }
             }
             *reinterpret_cast<VT*>(mine + v * VE) = q;
           }
