@@ -42,7 +42,7 @@ int go_axis_stream_c(const T* in, T* out, int64_t outer, int64_t n, int64_t inne
     ex->n_out_done = 1;
     if (EX == 1) {
       ex->done = 1;
-      ex->ppr = ex->row_len / N2;
+      ex->ppr = ex->row_len / (32 * VE);
     } else if (EX == 2) {
       ex->done = 1;
       ex->ppr = grid;
@@ -68,7 +68,9 @@ int pick_axis_ex(const T* in, T* out, int64_t outer, int64_t n, int64_t inner, i
                  int64_t k, const typename AccOf<T>::type* total, cudaStream_t s, PassExtra* ex) {
   const int kind = ex ? ex->kind : 0;
   if (kind == 1) {
-    if (ex->row_len % (32 * C) != 0 || inner % ex->row_len != 0) return -1;
+    if (ex->row_len % (32 * 16 / (int)sizeof(T)) != 0 || ex->row_len % (32 * C) != 0 ||
+        inner % ex->row_len != 0)
+      return -1;
     return pick_axis_k<T, Op, C, 1>(in, out, outer, n, inner, nout, k, total, s, ex);
   }
   if constexpr (!std::is_same<Op, OpMax>::value) {

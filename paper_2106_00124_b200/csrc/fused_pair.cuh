@@ -211,7 +211,10 @@ k_fused_pair(const T* __restrict__ in, T* __restrict__ out, int64_t outer, int64
         // warp reduction replaces the prefix/suffix scans (the float error
         // scales with the row total, inside the box-complement bound of
         // tests/parity.py); max has no inverse and keeps the scans below.
-        constexpr bool ADD_EXCL = MODE == ROW_EXCL && std::is_same<Op, OpAdd>::value;
+        // 8-byte rows with K2 >= 8 spill on this path (f64 512^3 box 16^3:
+        // 0.58 vs 0.53 ms), so they keep the sub-chunk scans below.
+        constexpr bool ADD_EXCL = MODE == ROW_EXCL && std::is_same<Op, OpAdd>::value &&
+                                  (sizeof(T) == 4 || K2 <= 4);
         if (MODE == ROW_WIN || (ADD_EXCL && kx == K2)) {
           T rtot = T(0);
           if constexpr (ADD_EXCL) {

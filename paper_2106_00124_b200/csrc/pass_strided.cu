@@ -459,14 +459,14 @@ int launch_axis_stream_i64max(const void*, void*, int64_t, int64_t, int64_t, int
                               cudaStream_t, PassExtra*);
 
 // EXSUM_AXIS_STREAM=0|1|2 (measurements): never / every eligible pass except
-// those folding row partials (default; the register butterfly of
-// k_strided_reg is faster there: the shared-memory fold needs two CTA
-// barriers per unit) / every eligible pass
+// those folding row partials / every eligible pass (default: with the
+// register butterfly the cp.async ring beats k_strided_reg there too, C4
+// row-partials pass 1.54 -> 1.42 ms)
 static int axis_stream_mode() {
   static int mode = -1;
   if (mode < 0) {
     const char* e = getenv("EXSUM_AXIS_STREAM");
-    mode = e ? atoi(e) : 1;
+    mode = e ? atoi(e) : 2;
   }
   return mode;
 }

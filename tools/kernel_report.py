@@ -28,6 +28,8 @@ CASES = {
     "c4": ((1024, 1024, 1024), "float32", [(16, 16, 16)], ["box-complement", "bdbsc", "bdbs"]),
     "c5": ((512, 512, 512), "float64", [(2, 2, 2), (8, 8, 8), (32, 32, 32), (128, 4, 1), (1, 1, 512)],
            ["bdbs", "bdbsc"]),
+    "c5bc": ((512, 512, 512), "float64", [(2, 2, 2), (8, 8, 8), (16, 16, 16)], ["box-complement"]),
+    "c4bc": ((1024, 1024, 1024), "float32", [(4, 4, 4), (8, 8, 8), (16, 16, 16)], ["box-complement"]),
 }
 
 
