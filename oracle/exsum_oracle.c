@@ -23,7 +23,11 @@
  * the reference's order).  The BDBSC total is a single sequential fold, as
  * in the reference.
  *
- * dtype codes: 0 = float32, 1 = float64, 2 = int64.  op codes: 0 = add, 1 = max.
+ *   - sat_included / sat_excluded included.py:37-121, excluded.py:83-85
+ *   - mod-add:<m> monoid           monoid.py:235-286 (op code 2, oracle_set_modulus)
+ *
+ * dtype codes: 0 = float32, 1 = float64, 2 = int64.  op codes: 0 = add, 1 = max,
+ * 2 = mod-add.
  * Return codes: 0 ok, 1 usage error, 2 configuration error.
  */
 #include <stdint.h>
@@ -56,18 +60,23 @@ static inline int64_t i64_add(int64_t a, int64_t b) { return (int64_t)((uint64_t
 static inline int64_t i64_sub(int64_t a, int64_t b) { return (int64_t)((uint64_t)a - (uint64_t)b); }
 
 /*
- * One instantiation per (type, operator).  C(a,b) is the monoid combine;
- * the reference applies it as np.add(dst, src) / np.maximum(dst, src), and
- * both are commutative, so operand order inside one combine never changes
- * the bits.
+ * One instantiation per (type, operator).  C(a,b) is the monoid combine
+ * (combine_into / rcombine_into); the reference applies it as np.add(dst, src)
+ * / np.maximum(dst, src), and both are commutative, so operand order inside
+ * one combine never changes the bits.  ACC(a,b) and FIN(v) restate
+ * MonoidOps.accumulate: a running ACC along the line, then FIN on every
+ * element of it (identity for the plain monoids; for mod-add a raw int64
+ * cumsum followed by np.remainder over the whole line, monoid.py:280-283,
+ * so even an element no combine touched comes out reduced).
  */
-#define DEFINE_ORACLE(SFX, T, C, IDENT)                                                        \
+#define DEFINE_ORACLE(SFX, T, C, ACC, FIN, IDENT)                                              \
     /* scan.py:61-102 -- in-place windowed sum of one strided line. */                         \
     static void win_line_##SFX(T *buf, int64_t n, int64_t stride, int64_t k, T *scratch) {    \
         if (n == 0 || k == 1) return;                                                          \
-        if (k >= n) { /* scan.py:66-68: reverse inclusive scan */                             \
+        if (k >= n) { /* scan.py:66-68: reverse inclusive scan (ops.accumulate) */            \
             for (int64_t x = n - 2; x >= 0; --x)                                               \
-                buf[x * stride] = C(buf[x * stride], buf[(x + 1) * stride]);                   \
+                buf[x * stride] = ACC(buf[x * stride], buf[(x + 1) * stride]);                 \
+            for (int64_t x = 0; x < n; ++x) buf[x * stride] = FIN(buf[x * stride]);            \
             return;                                                                            \
         }                                                                                      \
         for (int64_t x = 0; x < n; ++x) scratch[x] = buf[x * stride];                          \
@@ -110,10 +119,11 @@ static inline int64_t i64_sub(int64_t a, int64_t b) { return (int64_t)((uint64_t
         _Pragma("omp parallel for schedule(static)")                                           \
         for (int64_t c = 0; c < m; ++c) {                                                      \
             if (!reverse) {                                                                    \
-                for (int64_t x = 1; x < n; ++x) s[x * m + c] = C(s[(x - 1) * m + c], s[x * m + c]); \
+                for (int64_t x = 1; x < n; ++x) s[x * m + c] = ACC(s[(x - 1) * m + c], s[x * m + c]); \
             } else {                                                                           \
-                for (int64_t x = n - 2; x >= 0; --x) s[x * m + c] = C(s[(x + 1) * m + c], s[x * m + c]); \
+                for (int64_t x = n - 2; x >= 0; --x) s[x * m + c] = ACC(s[(x + 1) * m + c], s[x * m + c]); \
             }                                                                                  \
+            for (int64_t x = 0; x < n; ++x) s[x * m + c] = FIN(s[x * m + c]);                  \
         }                                                                                      \
     }                                                                                          \
                                                                                                \
@@ -125,7 +135,7 @@ static inline int64_t i64_sub(int64_t a, int64_t b) { return (int64_t)((uint64_t
     }                                                                                          \
                                                                                                \
     /* MonoidOps.fold: strict row-major left fold (monoid.py:161-164,200-204,229-232). */     \
-    static T fold_##SFX(const T *a, int64_t N) {                                               \
+    static inline T fold_##SFX(const T *a, int64_t N) {                                        \
         if (N == 0) return (T)(IDENT);                                                         \
         T acc = a[0];                                                                          \
         for (int64_t i = 1; i < N; ++i) acc = C(acc, a[i]);                                    \
@@ -231,14 +241,92 @@ static inline int64_t i64_sub(int64_t a, int64_t b) { return (int64_t)((uint64_t
         }                                                                                      \
     }
 
-#define C_FADD(a, b) ((a) + (b))
-#define C_IADD(a, b) i64_add((a), (b))
-#define C_MAX(a, b) ((a) >= (b) ? (a) : (b))
+/* mod-add:<m> (monoid.py:235-286): np.add / np.subtract on int64 (wrapping),
+ * then np.remainder, which for m > 0 is the floor modulus in [0, m). */
+static int64_t g_mod = 2;
+static inline int64_t floor_mod(int64_t v) {
+    int64_t r = v % g_mod;
+    return r < 0 ? r + g_mod : r;
+}
+static inline int64_t mod_add(int64_t a, int64_t b) { return floor_mod(i64_add(a, b)); }
+static inline int64_t mod_sub(int64_t a, int64_t b) { return floor_mod(i64_sub(a, b)); }
 
-DEFINE_ORACLE(f32_add, float, C_FADD, 0.0f)
-DEFINE_ORACLE(f64_add, double, C_FADD, 0.0)
-DEFINE_ORACLE(i64_add, int64_t, C_IADD, 0)
-DEFINE_ORACLE(i64_max, int64_t, C_MAX, INT64_MIN)
+#define C_FADD(a, b) ((a) + (b))
+#define C_FSUB(a, b) ((a) - (b))
+#define C_IADD(a, b) i64_add((a), (b))
+#define C_ISUB(a, b) i64_sub((a), (b))
+#define C_MAX(a, b) ((a) >= (b) ? (a) : (b))
+#define C_NOFIN(v) (v)
+
+DEFINE_ORACLE(f32_add, float, C_FADD, C_FADD, C_NOFIN, 0.0f)
+DEFINE_ORACLE(f64_add, double, C_FADD, C_FADD, C_NOFIN, 0.0)
+DEFINE_ORACLE(i64_add, int64_t, C_IADD, C_IADD, C_NOFIN, 0)
+DEFINE_ORACLE(i64_max, int64_t, C_MAX, C_MAX, C_NOFIN, INT64_MIN)
+DEFINE_ORACLE(i64_mod, int64_t, mod_add, i64_add, floor_mod, 0)
+
+/*
+ * Summed-area-table routes, invertible monoids only (included.py:37-121,
+ * excluded.py:83-85).  sat_build: copy, then ops.accumulate along axes
+ * 0..d-1 in order (sequential per line, like numpy).  sat_included: out[x]
+ * folds the 2^d corner terms of the identity-below / saturated-above query
+ * table in itertools.product((False, True), repeat=d) order -- the all-high
+ * corner is copied first, then each further term is combined (even number
+ * of low picks) or subtracted (odd) into out, exactly like the numpy
+ * combine_into / subtract_into sequence of sat_included.
+ */
+#define DEFINE_SAT(SFX, T, C, SUB, ACC, FIN, IDENT)                                            \
+    static void sat_build_##SFX(const T *in, T *s, int d, const int64_t *ext) {               \
+        int64_t N = prod_range(ext, 0, d);                                                     \
+        memcpy(s, in, sizeof(T) * (size_t)N);                                                  \
+        for (int a = 0; a < d; ++a) {                                                          \
+            int64_t outer = prod_range(ext, 0, a), n = ext[a], inner = prod_range(ext, a + 1, d); \
+            _Pragma("omp parallel for schedule(static)")                                       \
+            for (int64_t l = 0; l < outer * inner; ++l) {                                      \
+                T *line = s + (l / inner) * n * inner + (l % inner);                           \
+                for (int64_t x = 1; x < n; ++x)                                                \
+                    line[x * inner] = ACC(line[(x - 1) * inner], line[x * inner]);             \
+                for (int64_t x = 0; x < n; ++x) line[x * inner] = FIN(line[x * inner]);        \
+            }                                                                                  \
+        }                                                                                      \
+    }                                                                                          \
+    static int sat_included_##SFX(const T *in, T *out, int d, const int64_t *ext,             \
+                                  const int64_t *k) {                                          \
+        int64_t N = prod_range(ext, 0, d);                                                     \
+        T *s = (T *)malloc(sizeof(T) * (size_t)(N > 0 ? N : 1));                               \
+        if (!s) return ORC_USAGE;                                                              \
+        sat_build_##SFX(in, s, d, ext);                                                        \
+        int64_t str[16];                                                                       \
+        str[d - 1] = 1;                                                                        \
+        for (int j = d - 2; j >= 0; --j) str[j] = str[j + 1] * ext[j + 1];                     \
+        _Pragma("omp parallel for schedule(static)")                                           \
+        for (int64_t f = 0; f < N; ++f) {                                                      \
+            int64_t x[16];                                                                     \
+            int64_t r = f;                                                                     \
+            for (int j = d - 1; j >= 0; --j) { x[j] = r % ext[j]; r /= ext[j]; }               \
+            T acc = (T)(IDENT);                                                                \
+            for (int64_t p = 0; p < ((int64_t)1 << d); ++p) {                                  \
+                int64_t idx = 0, lows = 0, below = 0;                                          \
+                for (int j = 0; j < d; ++j) {                                                  \
+                    int lo = (int)((p >> (d - 1 - j)) & 1);                                    \
+                    int64_t c = lo ? x[j] - 1 : (x[j] + k[j] - 1 < ext[j] - 1 ? x[j] + k[j] - 1 : ext[j] - 1); \
+                    lows += lo;                                                                \
+                    if (c < 0) below = 1; else idx += c * str[j];                              \
+                }                                                                              \
+                T v = below ? (T)(IDENT) : s[idx];                                             \
+                if (p == 0) acc = v;                                                           \
+                else if (lows % 2 == 0) acc = C(acc, v);                                       \
+                else acc = SUB(acc, v);                                                        \
+            }                                                                                  \
+            out[f] = acc;                                                                      \
+        }                                                                                      \
+        free(s);                                                                               \
+        return ORC_OK;                                                                         \
+    }
+
+DEFINE_SAT(f32_add, float, C_FADD, C_FSUB, C_FADD, C_NOFIN, 0.0f)
+DEFINE_SAT(f64_add, double, C_FADD, C_FSUB, C_FADD, C_NOFIN, 0.0)
+DEFINE_SAT(i64_add, int64_t, C_IADD, C_ISUB, C_IADD, C_NOFIN, 0)
+DEFINE_SAT(i64_mod, int64_t, mod_add, mod_sub, i64_add, floor_mod, 0)
 
 /* ---------------------------------------------------------------- C ABI --- */
 
@@ -258,6 +346,7 @@ static int normalize(int d, const int64_t *ext, const int64_t *box, int64_t *k) 
         if (dtype == 1 && op == 0) { FN##_f64_add(__VA_ARGS__); break; }        \
         if (dtype == 2 && op == 0) { FN##_i64_add(__VA_ARGS__); break; }        \
         if (dtype == 2 && op == 1) { FN##_i64_max(__VA_ARGS__); break; }        \
+        if (dtype == 2 && op == 2) { FN##_i64_mod(__VA_ARGS__); break; }        \
         return ORC_CONFIG;                                                      \
     } while (0)
 
@@ -288,7 +377,7 @@ int oracle_bdbsc_excluded(const void *in, void *out, int dtype, int op, int d,
     int64_t k[16];
     int rc = normalize(d, ext, box, k);
     if (rc) return rc;
-    if (op != 0) return ORC_CONFIG;
+    if (op == 1) return ORC_CONFIG;
     set_threads(nthreads);
     int64_t N = prod_range(ext, 0, d);
     if (dtype == 0) {
@@ -303,11 +392,18 @@ int oracle_bdbsc_excluded(const void *in, void *out, int dtype, int op, int d,
         double total = fold_f64_add(in, N);
         double *o = out;
         for (int64_t i = 0; i < N; ++i) o[i] = total - o[i];
-    } else if (dtype == 2) {
+    } else if (dtype == 2 && op == 0) {
         bdbs_i64_add(in, out, d, ext, k);
         int64_t total = fold_i64_add(in, N);
         int64_t *o = out;
         for (int64_t i = 0; i < N; ++i) o[i] = i64_sub(total, o[i]);
+    } else if (dtype == 2 && op == 2) {
+        /* ModAddOps.fold: int(arr.sum()) % m (wrapping int64 sum, floor mod);
+         * rsubtract_scalar: np.subtract then np.remainder (monoid.py:274-286) */
+        bdbs_i64_mod(in, out, d, ext, k);
+        int64_t total = floor_mod(fold_i64_add(in, N));
+        int64_t *o = out;
+        for (int64_t i = 0; i < N; ++i) o[i] = mod_sub(total, o[i]);
     } else {
         return ORC_CONFIG;
     }
@@ -324,7 +420,55 @@ int oracle_box_complement_excluded(const void *in, void *out, int dtype, int op,
     if (dtype == 1 && op == 0) return box_complement_f64_add(in, out, d, ext, k);
     if (dtype == 2 && op == 0) return box_complement_i64_add(in, out, d, ext, k);
     if (dtype == 2 && op == 1) return box_complement_i64_max(in, out, d, ext, k);
+    if (dtype == 2 && op == 2) return box_complement_i64_mod(in, out, d, ext, k);
     return ORC_CONFIG;
+}
+
+/* mod-add:<m> modulus for op code 2 (2 <= m <= 2^31, monoid.py:27,250-256). */
+int oracle_set_modulus(int64_t m) {
+    if (m < 2 || m > ((int64_t)1 << 31)) return ORC_CONFIG;
+    g_mod = m;
+    return ORC_OK;
+}
+
+/* "sat" (included.py:98-121); needs an inverse, so max is a configuration error. */
+int oracle_sat_included(const void *in, void *out, int dtype, int op, int d,
+                        const int64_t *ext, const int64_t *box, int nthreads) {
+    int64_t k[16];
+    int rc = normalize(d, ext, box, k);
+    if (rc) return rc;
+    set_threads(nthreads);
+    if (dtype == 0 && op == 0) return sat_included_f32_add(in, out, d, ext, k);
+    if (dtype == 1 && op == 0) return sat_included_f64_add(in, out, d, ext, k);
+    if (dtype == 2 && op == 0) return sat_included_i64_add(in, out, d, ext, k);
+    if (dtype == 2 && op == 2) return sat_included_i64_mod(in, out, d, ext, k);
+    return ORC_CONFIG;
+}
+
+/* "satc" (excluded.py:83-85): fold(A) (-) sat_included(A), like bdbsc. */
+int oracle_satc_excluded(const void *in, void *out, int dtype, int op, int d,
+                         const int64_t *ext, const int64_t *box, int nthreads) {
+    int rc = oracle_sat_included(in, out, dtype, op, d, ext, box, nthreads);
+    if (rc) return rc;
+    int64_t N = prod_range(ext, 0, d);
+    if (dtype == 0) {
+        float total = fold_f32_add(in, N);
+        float *o = out;
+        for (int64_t i = 0; i < N; ++i) o[i] = total - o[i];
+    } else if (dtype == 1) {
+        double total = fold_f64_add(in, N);
+        double *o = out;
+        for (int64_t i = 0; i < N; ++i) o[i] = total - o[i];
+    } else if (op == 0) {
+        int64_t total = fold_i64_add(in, N);
+        int64_t *o = out;
+        for (int64_t i = 0; i < N; ++i) o[i] = i64_sub(total, o[i]);
+    } else {
+        int64_t total = floor_mod(fold_i64_add(in, N));
+        int64_t *o = out;
+        for (int64_t i = 0; i < N; ++i) o[i] = mod_sub(total, o[i]);
+    }
+    return ORC_OK;
 }
 
 int oracle_brute_included(const void *in, void *out, int dtype, int op, int d,
@@ -353,5 +497,6 @@ int oracle_fold(const void *in, int64_t n, int dtype, int op, void *result) {
     if (dtype == 1 && op == 0) { *(double *)result = fold_f64_add(in, n); return ORC_OK; }
     if (dtype == 2 && op == 0) { *(int64_t *)result = fold_i64_add(in, n); return ORC_OK; }
     if (dtype == 2 && op == 1) { *(int64_t *)result = fold_i64_max(in, n); return ORC_OK; }
+    if (dtype == 2 && op == 2) { *(int64_t *)result = floor_mod(fold_i64_add(in, n)); return ORC_OK; }
     return ORC_CONFIG;
 }

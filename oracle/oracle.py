@@ -14,6 +14,8 @@ reference itself (``tests/golden/make_golden.py``):
   ``bdbs_excluded`` (excluded.py:72-75,88-90) and ``box_complement_excluded``
   (excluded.py:129-159) with the reference's exact floating-point association,
   so it is bit-identical to the reference for every dtype.
+* ``sat_included`` / ``sat_excluded`` (included.py:37-121, excluded.py:83-85) and the
+  ``mod-add:<m>`` monoid (monoid.py:235-286) for every route (``op="mod-add:<m>"``).
 * ``brute_included`` / ``brute_excluded``: restatements of the brute-force
   ``oracle_included`` / ``oracle_excluded`` (oracle.py:37-71), in C for speed and
   in pure Python (``py_brute_*``) for tiny cases.
@@ -32,7 +34,7 @@ _HERE = os.path.dirname(os.path.abspath(__file__))
 _LIB_PATH = os.path.join(_HERE, "liboracle.so")
 
 DTYPE_CODES = {np.dtype(np.float32): 0, np.dtype(np.float64): 1, np.dtype(np.int64): 2}
-OP_CODES = {"add": 0, "max": 1}
+OP_CODES = {"add": 0, "max": 1, "mod-add": 2}
 IDENTITY = {
     ("add", np.dtype(np.float32)): np.float32(0.0),
     ("add", np.dtype(np.float64)): np.float64(0.0),
@@ -60,6 +62,8 @@ def lib():
             "oracle_bdbs_included",
             "oracle_bdbsc_excluded",
             "oracle_box_complement_excluded",
+            "oracle_sat_included",
+            "oracle_satc_excluded",
             "oracle_brute_included",
             "oracle_brute_excluded",
         ):
@@ -78,6 +82,8 @@ def lib():
             ctypes.c_void_p, ctypes.c_int64, ctypes.c_int, ctypes.c_int, ctypes.c_void_p,
         ]
         L.oracle_fold.restype = ctypes.c_int
+        L.oracle_set_modulus.argtypes = [ctypes.c_int64]
+        L.oracle_set_modulus.restype = ctypes.c_int
         _lib = L
     return _lib
 
@@ -87,10 +93,15 @@ class OracleError(RuntimeError):
 
 
 def _codes(arr: np.ndarray, op: str):
+    """op: "add", "max" or "mod-add:<m>" (sets the oracle's modulus)."""
     dt = DTYPE_CODES.get(arr.dtype)
-    if dt is None or op not in OP_CODES:
+    base, _, mod = op.partition(":")
+    if dt is None or base not in OP_CODES or (base == "mod-add") != bool(mod):
         raise OracleError(f"unsupported dtype/op {arr.dtype}/{op}")
-    return dt, OP_CODES[op]
+    if base == "mod-add":
+        if lib().oracle_set_modulus(int(mod)) != 0:
+            raise OracleError(f"bad modulus {mod}")
+    return dt, OP_CODES[base]
 
 
 def _i64(seq):
@@ -123,6 +134,14 @@ def box_complement_excluded(a, box, op="add", nthreads=0):
     return _run("oracle_box_complement_excluded", a, box, op, nthreads)
 
 
+def sat_included(a, box, op="add", nthreads=0):
+    return _run("oracle_sat_included", a, box, op, nthreads)
+
+
+def sat_excluded(a, box, op="add", nthreads=0):
+    return _run("oracle_satc_excluded", a, box, op, nthreads)
+
+
 def brute_included(a, box, op="add", nthreads=0):
     return _run("oracle_brute_included", a, box, op, nthreads)
 
@@ -135,6 +154,8 @@ ROUTES = {
     "bdbs": bdbs_included,
     "bdbsc": bdbs_excluded,
     "box-complement": box_complement_excluded,
+    "sat": sat_included,
+    "satc": sat_excluded,
 }
 
 
@@ -165,6 +186,9 @@ def fold(a, op="add"):
 def _combine(op):
     if op == "add":
         return lambda a, b: a + b
+    if op.startswith("mod-add:"):
+        m = int(op.split(":")[1])
+        return lambda a, b: (int(a) + int(b)) % m
     return lambda a, b: a if a >= b else b
 
 

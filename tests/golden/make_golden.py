@@ -2,7 +2,7 @@
 
 Run in the build container (where /root/reference exists):
 
-    python tests/golden/make_golden.py
+    python tests/golden/make_golden.py [--only-ext]
 
 It imports the unmodified reference package read-only from
 /root/reference/pkg/src (``exsum``), runs its public entry points
@@ -188,5 +188,117 @@ def make():
     print("wrote kat.npz, small.npz, medium.npz to", HERE)
 
 
+def make_ext():
+    """ext.npz: the section 8(f) rows -- "sat"/"satc" (included.py:37-121,
+    excluded.py:83-85) for the invertible monoids and the ``mod-add:<m>``
+    monoid (monoid.py:235-286) on every route, through the reference."""
+    ex = _import_reference()
+    from exsum.excluded import sat_excluded
+    from exsum.included import sat_included
+
+    class AddF32(ex.FloatAddOps):
+        name = "add-f32"
+        dtype = np.dtype(np.float32)
+        identity = np.float32(0.0)
+
+    routes = {
+        "bdbs": ex.bdbs_included,
+        "bdbsc": ex.bdbs_excluded,
+        "box-complement": ex.box_complement_excluded,
+        "sat": sat_included,
+        "satc": sat_excluded,
+    }
+
+    def mono(name):
+        if name == "add-f32":
+            return AddF32()
+        return ex.resolve_monoid(name)
+
+    out = {}
+    meta = []
+
+    def case(tag, arr, mname, box, route_names):
+        ops = mono(mname)
+        arr = np.ascontiguousarray(arr, dtype=ops.dtype)
+        key_in = f"{tag}/in"
+        out[key_in] = arr
+        for r in route_names:
+            t = ex.Tensor(ops, arr.copy())
+            res = routes[r](t, box).data.copy()
+            key = f"{tag}/{r}"
+            out[key] = res
+            meta.append({"key": key, "in": key_in, "mono": mname, "route": r, "box": list(box),
+                         "ext": list(arr.shape)})
+        if arr.size <= 400 and mname != "add-f32":
+            clipped = tuple(min(k, m) for k, m in zip(box, arr.shape))
+            flat = [v.item() for v in arr.reshape(-1)]
+            for kind, fn in (("inc", ex.oracle_included), ("exc", ex.oracle_excluded)):
+                key = f"{tag}/oracle_{kind}"
+                out[key] = np.array(fn(arr.shape, flat, clipped, ops.combine, ops.identity),
+                                    dtype=ops.dtype).reshape(arr.shape)
+                meta.append({"key": key, "in": key_in, "mono": mname, "route": "oracle_" + kind,
+                             "box": list(box), "ext": list(arr.shape)})
+
+    rng = np.random.default_rng(2106)
+    ci = 0
+    # small random instances, d = 1..4, every invertible monoid: sat + satc
+    for d, count in [(1, 12), (2, 16), (3, 16), (4, 8)]:
+        for _ in range(count):
+            while True:
+                ext = tuple(int(v) for v in rng.integers(1, 7, size=d))
+                if int(np.prod(ext)) <= 360:
+                    break
+            box = tuple(int(rng.integers(1, n + 2)) for n in ext)
+            ivals = rng.integers(0, 100, size=ext).astype(np.int64)
+            fvals = rng.random(ext)
+            case(f"s{ci}_i", ivals, "add-i64", box, ["sat", "satc"])
+            case(f"s{ci}_f", fvals, "add-f64", box, ["sat", "satc"])
+            case(f"s{ci}_g", fvals.astype(np.float32), "add-f32", box, ["sat", "satc"])
+            ci += 1
+    # mod-add: canonical inputs (generate_input style, bench.py:103-114) and
+    # non-canonical ones (negative, >= m, large), every route
+    mods = [2, 7, 11, 97, 1000003, 2**31]
+    every = list(routes)
+    for d, count in [(1, 10), (2, 14), (3, 14), (4, 6)]:
+        for _ in range(count):
+            while True:
+                ext = tuple(int(v) for v in rng.integers(1, 7, size=d))
+                if int(np.prod(ext)) <= 360:
+                    break
+            box = tuple(int(rng.integers(1, n + 2)) for n in ext)
+            m = mods[ci % len(mods)]
+            canon = rng.integers(0, 100, size=ext).astype(np.int64) % m
+            case(f"m{ci}_c", canon, f"mod-add:{m}", box, every)
+            raw = rng.integers(-3 * m, 3 * m, size=ext).astype(np.int64)
+            if ci % 3 == 0:
+                raw = raw + rng.integers(-2**40, 2**40, size=ext).astype(np.int64)
+            case(f"m{ci}_r", raw, f"mod-add:{m}", box, every)
+            ci += 1
+    # medium: C-like shapes for sat/satc and mod-add
+    r0 = np.random.default_rng(0)
+    case("c1sat", r0.random((96, 80)), "add-f64", (32, 32), ["sat", "satc"])
+    r0 = np.random.default_rng(0)
+    case("c3sat", r0.standard_normal((16, 16, 16), dtype=np.float32), "add-f32", (4, 4, 4),
+         ["sat"])
+    r0 = np.random.default_rng(0)
+    case("c2sat", r0.integers(-2**20, 2**20, size=(24, 20, 28), dtype=np.int64), "add-i64",
+         (8, 8, 8), ["sat", "satc"])
+    r0 = np.random.default_rng(0)
+    case("c5sat", r0.standard_normal((12, 10, 14, 9)), "add-f64", (3, 4, 2, 5), ["sat", "satc"])
+    r0 = np.random.default_rng(0)
+    case("mmed", r0.integers(0, 100, size=(20, 18, 22), dtype=np.int64) % 97, "mod-add:97",
+         (4, 4, 4), every)
+    r0 = np.random.default_rng(0)
+    case("mmed2", r0.integers(-2**31, 2**31, size=(40, 50), dtype=np.int64), f"mod-add:{2**31}",
+         (8, 1), every)
+    out["meta"] = np.frombuffer(json.dumps(meta).encode(), dtype=np.uint8)
+    np.savez_compressed(os.path.join(HERE, "ext.npz"), **out)
+    print("wrote ext.npz:", len(meta), "outputs")
+
+
 if __name__ == "__main__":
-    make()
+    if "--only-ext" in sys.argv:
+        make_ext()
+    else:
+        make()
+        make_ext()

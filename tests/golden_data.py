@@ -54,3 +54,20 @@ def medium_cases():
         m["in"] = z[f"{m['name']}/in/{m['mono']}"]
         m["out"] = z[m["key"]]
         yield m
+
+
+def mono_op(mono: str) -> str:
+    """Oracle / device operator string for a monoid name ("mod-add:<m>" passes through)."""
+    return mono if mono.startswith("mod-add:") else MONO_OP[mono]
+
+
+def ext_cases():
+    """Yield dicts (key, mono, route, box, ext, 'in', 'out') for ext.npz: the
+    sat/satc and mod-add vectors."""
+    z = load("ext")
+    meta = json.loads(bytes(z["meta"]).decode())
+    for m in meta:
+        m = dict(m)
+        m["out"] = z[m["key"]]
+        m["in"] = z[m["in"]]
+        yield m

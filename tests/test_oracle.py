@@ -8,7 +8,7 @@ association -- and agree with the brute-force oracle restatement.
 import numpy as np
 import pytest
 
-from golden_data import MONO_OP, load, medium_cases, small_cases
+from golden_data import MONO_OP, ext_cases, load, medium_cases, mono_op, small_cases
 from oracle import oracle as orc
 
 
@@ -103,3 +103,17 @@ def test_int64_wraps_like_numpy():
 def test_max_rejected_for_weak_route():
     with pytest.raises(orc.OracleError):
         orc.bdbs_excluded(np.zeros((3, 3), dtype=np.int64), (2, 2), "max")
+
+
+def test_ext_sat_and_mod_add_bit_exact():
+    """sat / satc (included.py:37-121, excluded.py:83-85) and mod-add:<m>
+    (monoid.py:235-286, incl. non-canonical inputs) against the reference."""
+    n = 0
+    brute = {"oracle_inc": orc.brute_included, "oracle_exc": orc.brute_excluded}
+    for m in ext_cases():
+        fn = brute.get(m["route"]) or orc.ROUTES[m["route"]]
+        got = fn(m["in"], tuple(m["box"]), mono_op(m["mono"]))
+        assert got.dtype == m["out"].dtype
+        assert np.array_equal(got.view(np.uint8), m["out"].view(np.uint8)), m["key"]
+        n += 1
+    assert n >= 1000
