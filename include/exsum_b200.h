@@ -35,21 +35,25 @@
 extern "C" {
 #endif
 
-#define EXSUM_ABI_VERSION 1
+#define EXSUM_ABI_VERSION 2
 
 /* element types (MonoidOps.dtype, monoid.py:40) */
 #define EXSUM_F32 0 /* add-f32 (test-side float32 FloatAddOps)      */
 #define EXSUM_F64 1 /* add-f64  FloatAddOps   monoid.py:167-204      */
-#define EXSUM_I64 2 /* add-i64 / max-i64      monoid.py:130-164,207-232 */
+#define EXSUM_I64 2 /* add-i64 / max-i64 / mod-add:<m>  monoid.py:130-164,207-286 */
 
 /* operators (MonoidOps.combine) */
 #define EXSUM_ADD 0
 #define EXSUM_MAX 1
+#define EXSUM_MODADD 2 /* mod-add:<m> ModAddOps monoid.py:235-286; int64, needs the
+                          modulus (2 <= m <= 2^31): only the exsum_route* calls take it */
 
 /* routes (bench.ALGORITHMS names, bench.py:60-76) */
 #define EXSUM_ROUTE_BDBS 0           /* "bdbs"           included.py:124-129 */
 #define EXSUM_ROUTE_BDBSC 1          /* "bdbsc"          excluded.py:88-90   */
 #define EXSUM_ROUTE_BOX_COMPLEMENT 2 /* "box-complement" excluded.py:129-159 */
+#define EXSUM_ROUTE_SAT 3            /* "sat"            included.py:98-121  */
+#define EXSUM_ROUTE_SATC 4           /* "satc"           excluded.py:83-85   */
 
 #define EXSUM_OK 0
 #define EXSUM_EUSAGE 1
@@ -69,6 +73,20 @@ const char *exsum_last_error(void);
  * (alloc.new_array, alloc.py:63-65; tensor.py:91-114; scan.py:70). */
 int exsum_workspace_bytes(int route, int dtype, int op, int d, const int64_t *ext,
                           const int64_t *box, size_t *bytes);
+
+/* Any route (EXSUM_ROUTE_*) with any operator, including mod-add:<m>
+ * (`modulus` is ignored for the other operators).  Replaces the registry slot
+ * `fn(t, box)` of every bench.ALGORITHMS entry on this path (bench.py:60-76):
+ * "bdbs", "bdbsc", "box-complement", "sat" (included.py:98-121) and "satc"
+ * (excluded.py:83-85).  bdbsc / sat / satc need an invertible operator
+ * (add, mod-add); max returns EXSUM_ECONFIG like bench.check_algorithm_config. */
+int exsum_route(int route, const void *in, void *out, int dtype, int op, int64_t modulus, int d,
+                const int64_t *ext, const int64_t *box, void *ws, size_t ws_bytes, void *stream);
+int exsum_route_workspace_bytes(int route, int dtype, int op, int64_t modulus, int d,
+                                const int64_t *ext, const int64_t *box, size_t *bytes);
+/* Host-buffer form of exsum_route (see exsum_run_host). */
+int exsum_route_host(int route, const void *h_in, void *h_out, int dtype, int op, int64_t modulus,
+                     int d, const int64_t *ext, const int64_t *box);
 
 /* Strong included sum, any monoid.  Replaces bdbs_included(t, box)
  * (included.py:124-129); bdbs_1d(ops, values, k) (scan.py:53-58) is d == 1. */

@@ -2,7 +2,8 @@
 
 Public names mirror the reference package ``exsum`` (pkg/src/exsum/__init__.py)
 for the accelerated path: ``bdbs_included``, ``bdbs_excluded``,
-``box_complement_excluded``, ``bdbs_1d``, ``windowed_sum_axis``, ``Tensor``,
+``box_complement_excluded``, ``sat_included``, ``sat_excluded``, ``bdbs_1d``,
+``windowed_sum_axis``, ``Tensor``,
 the monoids and the error types, plus the ``ALGORITHMS`` registry.  All
 arithmetic runs in hand-written sm_100a CUDA kernels (``csrc/``) behind the C
 ABI in ``include/exsum_b200.h``; there is no CPU fallback.
@@ -21,6 +22,7 @@ from .monoid import (
     FloatAddOps,
     IntAddOps,
     IntMaxOps,
+    ModAddOps,
     MonoidOps,
     resolve_monoid,
 )
@@ -34,6 +36,8 @@ from .routes import (
     check_algorithm_config,
     register_with_reference,
     resolve_algorithm,
+    sat_excluded,
+    sat_included,
     windowed_sum_axis,
 )
 from .tensor import Tensor, crop_to, normalize_box, pad_to_box_multiple, validate_extents
@@ -42,9 +46,11 @@ __version__ = "0.1.0"
 
 __all__ = [
     "ALGORITHMS", "AlgorithmInfo", "ConfigurationError", "DeviceError", "ExsumError",
-    "Float32AddOps", "FloatAddOps", "IntAddOps", "IntMaxOps", "MONOID_CHOICES", "MonoidOps",
+    "Float32AddOps", "FloatAddOps", "IntAddOps", "IntMaxOps", "MONOID_CHOICES", "ModAddOps",
+    "MonoidOps",
     "Tensor", "UsageError", "VerificationError", "bdbs_1d", "bdbs_excluded", "bdbs_included",
     "box_complement_excluded", "check_algorithm_config", "crop_to", "normalize_box",
     "pad_to_box_multiple", "register_with_reference", "resolve_algorithm", "resolve_monoid",
+    "sat_excluded", "sat_included",
     "validate_extents", "windowed_sum_axis",
 ]

@@ -21,13 +21,17 @@ LIB_PATH = os.environ.get("EXSUM_LIB") or os.path.join(
     os.path.dirname(os.path.abspath(__file__)), "libexsum_b200.so")
 
 DTYPE = {"float32": 0, "float64": 1, "int64": 2}
-OP = {"add": 0, "max": 1}
-ROUTE = {"bdbs": 0, "bdbsc": 1, "box-complement": 2}
+OP = {"add": 0, "max": 1, "mod-add": 2}
+ROUTE = {"bdbs": 0, "bdbsc": 1, "box-complement": 2, "sat": 3, "satc": 4}
+ABI_VERSION = 2
 
 EXPORTS = (
     "exsum_abi_version",
     "exsum_last_error",
     "exsum_workspace_bytes",
+    "exsum_route_workspace_bytes",
+    "exsum_route",
+    "exsum_route_host",
     "exsum_bdbs_included",
     "exsum_bdbsc_excluded",
     "exsum_box_complement_excluded",
@@ -78,6 +82,14 @@ def load():
         L.exsum_windowed_pass.restype = ci
         L.exsum_run_host.argtypes = [ci, vp, vp, ci, ci, ci, i64p, i64p]
         L.exsum_run_host.restype = ci
+        i64 = ctypes.c_int64
+        L.exsum_route_workspace_bytes.argtypes = [ci, ci, ci, i64, ci, i64p, i64p,
+                                                  ctypes.POINTER(sz)]
+        L.exsum_route_workspace_bytes.restype = ci
+        L.exsum_route.argtypes = [ci, vp, vp, ci, ci, i64, ci, i64p, i64p, vp, sz, vp]
+        L.exsum_route.restype = ci
+        L.exsum_route_host.argtypes = [ci, vp, vp, ci, ci, i64, ci, i64p, i64p]
+        L.exsum_route_host.restype = ci
         L.exsum_release_cache.restype = ci
         L.exsum_profile_enable.argtypes = [ci]
         L.exsum_profile_enable.restype = ci
@@ -95,7 +107,7 @@ def load():
             fn = getattr(L, name)
             fn.argtypes = [vp, vp, ci, ci, ci, i64p, i64p, vp, vp, sz, vp]
             fn.restype = ci
-        if L.exsum_abi_version() != 1:
+        if L.exsum_abi_version() != ABI_VERSION:
             raise DeviceError("libexsum_b200.so ABI version mismatch")
         _lib = L
         return L
@@ -116,10 +128,11 @@ def check(rc: int) -> None:
     raise DeviceError(msg or f"native call failed with code {rc}")
 
 
-def workspace_bytes(route: str, dtype: str, op: str, ext, box) -> int:
+def workspace_bytes(route: str, dtype: str, op: str, ext, box, modulus: int = 0) -> int:
     out = ctypes.c_size_t(0)
-    check(load().exsum_workspace_bytes(ROUTE[route], DTYPE[dtype], OP[op], len(ext),
-                                       i64_array(ext), i64_array(box), ctypes.byref(out)))
+    check(load().exsum_route_workspace_bytes(ROUTE[route], DTYPE[dtype], OP[op], int(modulus),
+                                             len(ext), i64_array(ext), i64_array(box),
+                                             ctypes.byref(out)))
     return int(out.value)
 
 

@@ -7,6 +7,10 @@
 //                                          into the last pass's stores
 //   box-complement  excluded.py:129-159   slab decomposition, peeling the LAST
 //                                          axis first (see below)
+//   sat / satc      included.py:37-121,   running-sum table (d sequential
+//                   excluded.py:83-85     scans) + one 2^d-corner query (sat.cu)
+//   mod-add:<m>     monoid.py:235-286     any route: canonical residues, the
+//                                          exact int64 + route, a mod-m epilogue
 //
 // Box-complement order.  The reference peels dimension 0 first: round i adds
 // the "below"/"above" slabs of dimension i on the reduced slice.  The slab
@@ -113,12 +117,19 @@ int normalize(int d, const int64_t* ext, const int64_t* box, Shape* s) {
   return EXSUM_OK;
 }
 
-int check_types(int dtype, int op) {
+int check_types(int dtype, int op, int64_t modulus = 0) {
   if (dtype != EXSUM_F32 && dtype != EXSUM_F64 && dtype != EXSUM_I64)
     return fail(EXSUM_ECONFIG, "unsupported dtype (float32, float64, int64)");
-  if (op != EXSUM_ADD && op != EXSUM_MAX) return fail(EXSUM_ECONFIG, "unsupported operator");
+  if (op != EXSUM_ADD && op != EXSUM_MAX && op != EXSUM_MODADD)
+    return fail(EXSUM_ECONFIG, "unsupported operator");
   if (op == EXSUM_MAX && dtype != EXSUM_I64)
     return fail(EXSUM_ECONFIG, "max is provided for int64 only (max-i64, monoid.py:207-232)");
+  if (op == EXSUM_MODADD) {
+    if (dtype != EXSUM_I64) return fail(EXSUM_ECONFIG, "mod-add is an int64 monoid (monoid.py:235-248)");
+    // ModAddOps.__init__ (monoid.py:250-256): 2 <= m <= 2^31
+    if (modulus < 2 || modulus > ((int64_t)1 << 31))
+      return fail(EXSUM_ECONFIG, "mod-add modulus must be in [2, 2147483648]");
+  }
   return EXSUM_OK;
 }
 
@@ -364,8 +375,172 @@ int route_box_complement(const Shape& s, int dtype, int op, const void* src, voi
   return bc_finish(s, dtype, op, src, dst, T, head, fused, &ex0, reduce_and_tail, ar, st, launches);
 }
 
-int dispatch(int route, const Shape& s, int dtype, int op, const void* in, void* out, Arena& ar,
-             cudaStream_t st, int* launches) {
+// Running sum along the middle axis of [outer, n, inner] (np.add.accumulate),
+// src -> dst (in place allowed).  Lines are scanned sequentially (numpy's
+// association) unless there are too few of them to fill the GPU; then the
+// axis is cut into segments: local scans, an (in-place, recursive) scan of
+// the segment totals, and a carry pass.
+int scan_view(int dtype, const void* src, void* dst, int64_t outer, int64_t n, int64_t inner,
+              Arena& ar, cudaStream_t st, int* launches) {
+  const size_t es = dtype_size(dtype);
+  const bool live = ar.base != nullptr;
+  const int64_t ve = (int64_t)(16 / es);
+  const int64_t lanes = inner == 1 ? outer : outer * (inner % ve == 0 ? inner / ve : inner);
+  const int64_t want = (int64_t)num_sms() * 256;
+  int64_t L = n, nseg = 1;
+  if (lanes < want && n >= 4096) {
+    nseg = (want + lanes - 1) / lanes;
+    if (nseg > n / 1024) nseg = n / 1024;
+    L = ((n + nseg - 1) / nseg + 31) / 32 * 32;
+    nseg = (n + L - 1) / L;
+  }
+  if (live) {
+    ProfScope ps("sat_scan", 2.0 * (double)(outer * n * inner) * es, st);
+    *launches += launch_scan(dtype, src, dst, outer, n, inner, L, nseg, st);
+  }
+  if (nseg > 1) {
+    void* tot = ar.take((size_t)(outer * (nseg - 1) * inner) * es);
+    if (live) *launches += launch_seg_carry(dtype, dst, tot, outer, n, inner, L, nseg, 0, st);
+    int rc = scan_view(dtype, tot, tot, outer, nseg - 1, inner, ar, st, launches);
+    if (rc) return rc;
+    if (live) *launches += launch_seg_carry(dtype, dst, tot, outer, n, inner, L, nseg, 1, st);
+  }
+  return EXSUM_OK;
+}
+
+// "sat" / "satc" (included.py:98-121, excluded.py:83-85) on an invertible +
+// monoid: the running-sum table in workspace, then the 2^d-corner query with
+// the route epilogue.  `total` (satc) comes from the caller when given.
+int route_sat(const Shape& s, int dtype, const void* in, void* out, Arena& ar, int qmode,
+              const void* given_total, const FastMod& fm, cudaStream_t st, int* launches) {
+  const size_t es = dtype_size(dtype);
+  const bool live = ar.base != nullptr;
+  const void* table = in;
+  void* S = nullptr;
+  bool have_table = false;
+  for (int a = 0; a < s.d; ++a) {
+    if (s.ext[a] == 1) continue;  // accumulate over one element is a copy
+    if (!have_table) S = ar.take((size_t)s.N * es);
+    have_table = true;
+    int rc = scan_view(dtype, table, S, prod(s.ext, 0, a), s.ext[a], prod(s.ext, a + 1, s.d), ar,
+                       st, launches);
+    if (rc) return rc;
+    table = S;
+  }
+  const void* total = given_total;
+  if (qmode == QUERY_COMPLEMENT && !total) {
+    void* partials = ar.take((size_t)reduce_partials_count() * 8);
+    void* t = ar.take(8);
+    if (live) {
+      ProfScope ps("total", (double)s.N * es, st);
+      *launches += launch_total(dtype, EXSUM_ADD, in, s.N, partials, t, st);
+    }
+    total = t;
+  }
+  if (live) {
+    QShape q;
+    q.d = s.d;
+    int64_t stride = 1;
+    for (int j = s.d - 1; j >= 0; --j) {
+      q.ext[j] = s.ext[j];
+      q.k[j] = s.k[j];
+      q.str[j] = stride;
+      stride *= s.ext[j];
+    }
+    ProfScope ps("sat_query", 2.0 * (double)s.N * es, st);
+    *launches += launch_sat_query(dtype, table, out, q, s.N, total, qmode, fm, st);
+  }
+  return EXSUM_OK;
+}
+
+// mod-add:<m> (monoid.py:235-286).  Every route of the reference yields
+// (the exact integer fold) mod m, with one exception: elements that no
+// combine of bdbs touched keep their raw input value (windowed_sum_axis
+// leaves the last element of a line alone for 1 < k < n and the whole line
+// for k == 1; an accumulate, k >= n, reduces every element).  So: canonical
+// residues (int64 sums of N < 2^32 residues below 2^31 cannot overflow),
+// the exact int64 + route, then the mod-m epilogue, and the raw slice copied
+// back for bdbs / bdbsc.  The bdbsc / satc total is the wrapping int64 sum of
+// the raw input, reduced mod m (ModAddOps.fold: int(arr.sum()) % m).
+int route_modadd(int route, const Shape& s, int64_t modulus, const void* in, void* out, Arena& ar,
+                 cudaStream_t st, int* launches) {
+  const bool live = ar.base != nullptr;
+  const FastMod fm = make_fastmod(modulus);
+  const size_t bytes = (size_t)s.N * 8;
+  void* total = nullptr;
+  if (route == EXSUM_ROUTE_BDBSC || route == EXSUM_ROUTE_SATC) {
+    void* partials = ar.take((size_t)reduce_partials_count() * 8);
+    total = ar.take(8);
+    if (live) {
+      ProfScope ps("total", (double)bytes, st);
+      *launches += launch_total(EXSUM_I64, EXSUM_ADD, in, s.N, partials, total, st);
+    }
+  }
+  bool all_k1 = true, accumulated = false;
+  SliceSpec sp;
+  sp.d = s.d;
+  int64_t slice = 1;
+  for (int j = 0; j < s.d; ++j) {
+    sp.ext[j] = s.ext[j];
+    sp.fixed[j] = s.k[j] > 1;
+    if (s.k[j] > 1) all_k1 = false;
+    if (s.k[j] > 1 && s.k[j] >= s.ext[j]) accumulated = true;
+    if (s.k[j] == 1) slice *= s.ext[j];
+  }
+  const bool raw_route = route == EXSUM_ROUTE_BDBS || route == EXSUM_ROUTE_BDBSC;
+  if (raw_route && all_k1) {  // bdbs is a plain copy: nothing is reduced
+    if (live) {
+      ProfScope ps(route == EXSUM_ROUTE_BDBS ? "copy" : "mod_map", 2.0 * (double)bytes, st);
+      if (route == EXSUM_ROUTE_BDBS) {
+        cudaMemcpyAsync(out, in, bytes, cudaMemcpyDeviceToDevice, st);
+      } else {
+        *launches += launch_mod_map(in, out, s.N, 1, fm, total, st);
+      }
+    }
+    return EXSUM_OK;
+  }
+  void* canon = ar.take(bytes);
+  if (live) {
+    ProfScope ps("mod_map", 2.0 * (double)bytes, st);
+    *launches += launch_mod_map(in, canon, s.N, 0, fm, nullptr, st);
+  }
+  int rc = EXSUM_OK;
+  switch (route) {
+    case EXSUM_ROUTE_SAT:
+    case EXSUM_ROUTE_SATC:
+      return route_sat(s, EXSUM_I64, canon, out, ar,
+                       route == EXSUM_ROUTE_SAT ? QUERY_MOD : QUERY_MOD_COMPLEMENT, total, fm, st,
+                       launches);
+    case EXSUM_ROUTE_BOX_COMPLEMENT:
+      rc = route_box_complement(s, EXSUM_I64, EXSUM_ADD, canon, out, ar, st, launches);
+      break;
+    default:
+      rc = route_bdbs(s, EXSUM_I64, EXSUM_ADD, canon, out, ar, false, st, launches);
+      break;
+  }
+  if (rc) return rc;
+  if (!live) return EXSUM_OK;
+  // bdbs: reduce, then put the untouched raw elements back; bdbsc: the
+  // complement reads them raw (np.subtract(total, dst) then np.remainder)
+  auto raw_slice = [&]() {
+    if (raw_route && !accumulated) {
+      ProfScope ps("copy_slice", 2.0 * (double)slice * 8, st);
+      *launches += launch_copy_slice(in, out, sp, slice, st);
+    }
+  };
+  if (route == EXSUM_ROUTE_BDBSC) raw_slice();
+  {
+    ProfScope ps("mod_map", 2.0 * (double)bytes, st);
+    *launches += launch_mod_map(out, out, s.N, route == EXSUM_ROUTE_BDBSC ? 1 : 0, fm, total, st);
+  }
+  if (route == EXSUM_ROUTE_BDBS) raw_slice();
+  return EXSUM_OK;
+}
+
+int dispatch(int route, const Shape& s, int dtype, int op, int64_t modulus, const void* in,
+             void* out, Arena& ar, cudaStream_t st, int* launches) {
+  if (op == EXSUM_MODADD) return route_modadd(route, s, modulus, in, out, ar, st, launches);
+  const FastMod fm = make_fastmod(2);
   switch (route) {
     case EXSUM_ROUTE_BDBS:
       return route_bdbs(s, dtype, op, in, out, ar, false, st, launches);
@@ -373,41 +548,49 @@ int dispatch(int route, const Shape& s, int dtype, int op, const void* in, void*
       return route_bdbs(s, dtype, op, in, out, ar, true, st, launches);
     case EXSUM_ROUTE_BOX_COMPLEMENT:
       return route_box_complement(s, dtype, op, in, out, ar, st, launches);
+    case EXSUM_ROUTE_SAT:
+      return route_sat(s, dtype, in, out, ar, QUERY_PLAIN, nullptr, fm, st, launches);
+    case EXSUM_ROUTE_SATC:
+      return route_sat(s, dtype, in, out, ar, QUERY_COMPLEMENT, nullptr, fm, st, launches);
   }
   return fail(EXSUM_ECONFIG, "unknown route");
 }
 
-int validate(int route, int dtype, int op, int d, const int64_t* ext, const int64_t* box,
-             Shape* s) {
-  int rc = check_types(dtype, op);
+int validate(int route, int dtype, int op, int64_t modulus, int d, const int64_t* ext,
+             const int64_t* box, Shape* s) {
+  int rc = check_types(dtype, op, modulus);
   if (rc) return rc;
-  if (route < 0 || route > 2) return fail(EXSUM_ECONFIG, "unknown route");
-  // bench.check_algorithm_config (bench.py:88-100): weak route needs an inverse
-  if (route == EXSUM_ROUTE_BDBSC && op == EXSUM_MAX)
-    return fail(EXSUM_ECONFIG, "algorithm 'bdbsc' requires an invertible monoid, but 'max-i64' has no inverse");
+  if (route < 0 || route > EXSUM_ROUTE_SATC) return fail(EXSUM_ECONFIG, "unknown route");
+  // bench.check_algorithm_config (bench.py:88-100): bdbsc, sat and satc need
+  // an inverse (bench.py:61-69, needs_inverse)
+  if (op == EXSUM_MAX && route != EXSUM_ROUTE_BDBS && route != EXSUM_ROUTE_BOX_COMPLEMENT) {
+    const char* name = route == EXSUM_ROUTE_BDBSC ? "bdbsc" : route == EXSUM_ROUTE_SAT ? "sat" : "satc";
+    return fail(EXSUM_ECONFIG, std::string("algorithm '") + name +
+                                   "' requires an invertible monoid, but 'max-i64' has no inverse");
+  }
   return normalize(d, ext, box, s);
 }
 
 thread_local int g_last_launches = 0;
 thread_local long long g_total_launches = 0;
 
-int run_device(int route, const void* in, void* out, int dtype, int op, int d, const int64_t* ext,
-               const int64_t* box, void* ws, size_t ws_bytes, void* stream) {
+int run_device(int route, const void* in, void* out, int dtype, int op, int64_t modulus, int d,
+               const int64_t* ext, const int64_t* box, void* ws, size_t ws_bytes, void* stream) {
   g_err.clear();
   Shape s;
-  int rc = validate(route, dtype, op, d, ext, box, &s);
+  int rc = validate(route, dtype, op, modulus, d, ext, box, &s);
   if (rc) return rc;
   if (!in || !out) return fail(EXSUM_EUSAGE, "null array pointer");
   if (in == out) return fail(EXSUM_EUSAGE, "out must not alias in");
   Arena sizing(nullptr);
   int launches = 0;
-  rc = dispatch(route, s, dtype, op, in, out, sizing, (cudaStream_t)stream, &launches);
+  rc = dispatch(route, s, dtype, op, modulus, in, out, sizing, (cudaStream_t)stream, &launches);
   if (rc) return rc;
   if (sizing.off > 0 && (ws == nullptr || ws_bytes < sizing.off))
     return fail(EXSUM_EUSAGE, "workspace too small (see exsum_workspace_bytes)");
   Arena ar(ws);
   launches = 0;
-  rc = dispatch(route, s, dtype, op, in, out, ar, (cudaStream_t)stream, &launches);
+  rc = dispatch(route, s, dtype, op, modulus, in, out, ar, (cudaStream_t)stream, &launches);
   if (rc) return rc;
   g_last_launches = launches;
   g_total_launches += launches;
@@ -587,34 +770,44 @@ int exsum_last_launch_count(void) { return g_last_launches; }
 
 long long exsum_total_launch_count(void) { return g_total_launches; }
 
-int exsum_workspace_bytes(int route, int dtype, int op, int d, const int64_t* ext,
-                          const int64_t* box, size_t* bytes) {
+int exsum_route_workspace_bytes(int route, int dtype, int op, int64_t modulus, int d,
+                                const int64_t* ext, const int64_t* box, size_t* bytes) {
   g_err.clear();
   Shape s;
-  int rc = validate(route, dtype, op, d, ext, box, &s);
+  int rc = validate(route, dtype, op, modulus, d, ext, box, &s);
   if (rc) return rc;
   Arena sizing(nullptr);
   int launches = 0;
-  rc = dispatch(route, s, dtype, op, (const void*)1, (void*)2, sizing, nullptr, &launches);
+  rc = dispatch(route, s, dtype, op, modulus, (const void*)1, (void*)2, sizing, nullptr, &launches);
   if (rc) return rc;
   if (bytes) *bytes = sizing.off;
   return EXSUM_OK;
 }
 
+int exsum_workspace_bytes(int route, int dtype, int op, int d, const int64_t* ext,
+                          const int64_t* box, size_t* bytes) {
+  return exsum_route_workspace_bytes(route, dtype, op, 0, d, ext, box, bytes);
+}
+
+int exsum_route(int route, const void* in, void* out, int dtype, int op, int64_t modulus, int d,
+                const int64_t* ext, const int64_t* box, void* ws, size_t ws_bytes, void* stream) {
+  return run_device(route, in, out, dtype, op, modulus, d, ext, box, ws, ws_bytes, stream);
+}
+
 int exsum_bdbs_included(const void* in, void* out, int dtype, int op, int d, const int64_t* ext,
                         const int64_t* box, void* ws, size_t ws_bytes, void* stream) {
-  return run_device(EXSUM_ROUTE_BDBS, in, out, dtype, op, d, ext, box, ws, ws_bytes, stream);
+  return run_device(EXSUM_ROUTE_BDBS, in, out, dtype, op, 0, d, ext, box, ws, ws_bytes, stream);
 }
 
 int exsum_bdbsc_excluded(const void* in, void* out, int dtype, int op, int d, const int64_t* ext,
                          const int64_t* box, void* ws, size_t ws_bytes, void* stream) {
-  return run_device(EXSUM_ROUTE_BDBSC, in, out, dtype, op, d, ext, box, ws, ws_bytes, stream);
+  return run_device(EXSUM_ROUTE_BDBSC, in, out, dtype, op, 0, d, ext, box, ws, ws_bytes, stream);
 }
 
 int exsum_box_complement_excluded(const void* in, void* out, int dtype, int op, int d,
                                   const int64_t* ext, const int64_t* box, void* ws,
                                   size_t ws_bytes, void* stream) {
-  return run_device(EXSUM_ROUTE_BOX_COMPLEMENT, in, out, dtype, op, d, ext, box, ws, ws_bytes,
+  return run_device(EXSUM_ROUTE_BOX_COMPLEMENT, in, out, dtype, op, 0, d, ext, box, ws, ws_bytes,
                     stream);
 }
 
@@ -644,15 +837,15 @@ int exsum_windowed_pass(const void* in, void* out, int dtype, int op, int d, con
   return cuda_check("kernel launch");
 }
 
-int exsum_run_host(int route, const void* h_in, void* h_out, int dtype, int op, int d,
-                   const int64_t* ext, const int64_t* box) {
+int exsum_route_host(int route, const void* h_in, void* h_out, int dtype, int op, int64_t modulus,
+                     int d, const int64_t* ext, const int64_t* box) {
   g_err.clear();
   Shape s;
-  int rc = validate(route, dtype, op, d, ext, box, &s);
+  int rc = validate(route, dtype, op, modulus, d, ext, box, &s);
   if (rc) return rc;
   if (!h_in || !h_out) return fail(EXSUM_EUSAGE, "null host pointer");
   size_t ws_bytes = 0;
-  rc = exsum_workspace_bytes(route, dtype, op, d, ext, box, &ws_bytes);
+  rc = exsum_route_workspace_bytes(route, dtype, op, modulus, d, ext, box, &ws_bytes);
   if (rc) return rc;
   int dev = 0;
   if (cudaGetDevice(&dev) != cudaSuccess) return cuda_check("cudaGetDevice");
@@ -676,12 +869,17 @@ int exsum_run_host(int route, const void* h_in, void* h_out, int dtype, int op, 
     return fail(EXSUM_ECUDA, "cudaMalloc failed for host-path buffers");
   cudaStream_t st = c.stream[slot];
   cudaMemcpyAsync(c.in[slot].p, h_in, bytes, cudaMemcpyHostToDevice, st);
-  rc = run_device(route, c.in[slot].p, c.out[slot].p, dtype, op, d, ext, box, c.ws[slot].p,
-                  c.ws[slot].cap, st);
+  rc = run_device(route, c.in[slot].p, c.out[slot].p, dtype, op, modulus, d, ext, box,
+                  c.ws[slot].p, c.ws[slot].cap, st);
   if (rc) return rc;
   cudaMemcpyAsync(h_out, c.out[slot].p, bytes, cudaMemcpyDeviceToHost, st);
   if (cudaStreamSynchronize(st) != cudaSuccess) return cuda_check("cudaStreamSynchronize");
   return cuda_check("host path");
+}
+
+int exsum_run_host(int route, const void* h_in, void* h_out, int dtype, int op, int d,
+                   const int64_t* ext, const int64_t* box) {
+  return exsum_route_host(route, h_in, h_out, dtype, op, 0, d, ext, box);
 }
 
 int exsum_profile_enable(int on) {

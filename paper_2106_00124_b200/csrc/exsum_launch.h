@@ -82,6 +82,60 @@ int launch_fused_pair(int dtype, int op, const void* in, void* out, int64_t oute
                       int64_t n2, int64_t k1, int64_t k2, int mode, const void* total,
                       const void* Tail, cudaStream_t s);
 
+// ---------------------------------------------- sat / satc / mod-add (sat.cu)
+
+// Inclusive running sum (np.add.accumulate) along the middle axis of
+// [outer, n, inner], restarted every L elements (nseg = ceil(n / L) segments;
+// nseg == 1: plain sequential scan).  in == out is allowed.
+int launch_scan(int dtype, const void* in, void* out, int64_t outer, int64_t n, int64_t inner,
+                int64_t L, int64_t nseg, cudaStream_t s);
+// Segmented scans: step 0 gathers the segment totals into tot[outer, nseg-1,
+// inner]; step 1 adds the scanned totals back as carries.
+int launch_seg_carry(int dtype, void* out, void* tot, int64_t outer, int64_t n, int64_t inner,
+                     int64_t L, int64_t nseg, int step, cudaStream_t s);
+
+#define EXSUM_QMAX 32
+struct QShape {
+  int d;
+  int64_t ext[EXSUM_QMAX];
+  int64_t k[EXSUM_QMAX];
+  int64_t str[EXSUM_QMAX];
+};
+enum { QUERY_PLAIN = 0, QUERY_COMPLEMENT = 1, QUERY_MOD = 2, QUERY_MOD_COMPLEMENT = 3 };
+
+// floor modulus by a runtime m in [2, 2^31]: inv = floor((2^64 - 1) / m).
+struct FastMod {
+  unsigned long long m;
+  unsigned long long inv;
+};
+inline FastMod make_fastmod(int64_t m) {
+  FastMod f;
+  f.m = (unsigned long long)(m > 1 ? m : 2);
+  f.inv = ~0ULL / f.m;
+  return f;
+}
+
+// out = the 2^d-corner query of the running-sum table S (included.py:98-121)
+// with the route epilogue `mode` (total: Acc* for QUERY_COMPLEMENT, int64*
+// for QUERY_MOD_COMPLEMENT).
+int launch_sat_query(int dtype, const void* S, void* out, const QShape& q, int64_t N,
+                     const void* total, int mode, const FastMod& fm, cudaStream_t s);
+
+// mod-add element maps on int64: mode 0 out = in mod m (in may equal out);
+// mode 1 out = ((total mod m) - in) mod m.
+int launch_mod_map(const void* in, void* out, int64_t N, int mode, const FastMod& fm,
+                   const void* total, cudaStream_t s);
+
+struct SliceSpec {
+  int d;
+  int64_t ext[EXSUM_QMAX];
+  int fixed[EXSUM_QMAX];
+};
+// out[x] = in[x] for x with x_j = n_j - 1 on every fixed axis (count = the
+// product of the free extents).
+int launch_copy_slice(const void* in, void* out, const SliceSpec& sp, int64_t count,
+                      cudaStream_t s);
+
 size_t dtype_size(int dtype);
 int num_sms();
 

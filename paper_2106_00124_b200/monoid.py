@@ -16,6 +16,7 @@ add-i64    IntAddOps :130-164   int64        0             yes (wraps)
 add-f64    FloatAddOps :167-204 float64      0.0           yes
 add-f32    (new)   float32      0.0           yes
 max-i64    IntMaxOps :207-232   int64        INT64_MIN     no
+mod-add:m  ModAddOps :235-286   int64        0             yes (mod m)
 =========  ===================  ===========  ============  ==========
 
 Any object with ``name``/``dtype`` matching one of these (for example the
@@ -107,17 +108,55 @@ class IntMaxOps(MonoidOps):
         return a if a >= b else b
 
 
+MOD_ADD_MAX_MODULUS = 2**31  # monoid.py:27: keeps raw int64 partial sums overflow-free
+
+
+class ModAddOps(MonoidOps):
+    """Addition modulo m (2 <= m <= 2**31), values canonicalized to [0, m)
+    by every combine (monoid.py:235-286)."""
+
+    dtype = np.dtype(np.int64)
+    identity = 0
+    has_inverse = True
+    op = "mod-add"
+
+    def __init__(self, modulus: int):
+        if not isinstance(modulus, (int, np.integer)) or isinstance(modulus, bool):
+            raise ConfigurationError("mod-add modulus must be an integer")
+        modulus = int(modulus)
+        if not 2 <= modulus <= MOD_ADD_MAX_MODULUS:
+            raise ConfigurationError(
+                f"mod-add modulus must be in [2, {MOD_ADD_MAX_MODULUS}], got {modulus}"
+            )
+        self.modulus = modulus
+        self.name = f"mod-add:{modulus}"
+
+    def combine(self, a, b):
+        return (int(a) + int(b)) % self.modulus
+
+    def subtract(self, a, b):
+        return (int(a) - int(b)) % self.modulus
+
+
 def _wrap64(v: int) -> int:
     v &= (1 << 64) - 1
     return v - (1 << 64) if v >= 1 << 63 else v
 
 
 MONOIDS = {cls.name: cls for cls in (IntAddOps, FloatAddOps, Float32AddOps, IntMaxOps)}
-MONOID_CHOICES = tuple(MONOIDS)
+MONOID_CHOICES = tuple(MONOIDS) + ("mod-add:<m>",)
 
 
 def resolve_monoid(name: str) -> MonoidOps:
-    """Name -> monoid instance (monoid.py:362-385)."""
+    """Name -> monoid instance (monoid.py:362-385): add-i64, add-f64, add-f32,
+    max-i64 or mod-add:<m>."""
+    if isinstance(name, str) and name.startswith("mod-add:"):
+        text = name.split(":", 1)[1]
+        try:
+            modulus = int(text)
+        except ValueError:
+            raise ConfigurationError(f"bad mod-add modulus: {text!r}") from None
+        return ModAddOps(modulus)
     cls = MONOIDS.get(name)
     if cls is None:
         raise ConfigurationError(
@@ -136,9 +175,15 @@ def unwrap(ops):
 
 
 def device_operator(ops):
-    """(dtype, op) for the device library, or ConfigurationError -- before any work."""
+    """(dtype, op, has_inverse) for the device library, or ConfigurationError --
+    before any work.  For mod-add the modulus is ``modulus_of(ops)``."""
     base = unwrap(ops)
     name = getattr(base, "name", None)
+    if isinstance(name, str) and name.startswith("mod-add:"):
+        modulus_of(base)  # validates like ModAddOps.__init__
+        if np.dtype(getattr(base, "dtype", np.int64)) != np.dtype(np.int64):
+            raise ConfigurationError(f"monoid {name!r} must be int64")
+        return np.dtype(np.int64), "mod-add", True
     cls = MONOIDS.get(name)
     if cls is None:
         raise ConfigurationError(
@@ -148,3 +193,21 @@ def device_operator(ops):
     if dtype != cls.dtype:
         raise ConfigurationError(f"monoid {name!r} with dtype {dtype} has no B200 kernel")
     return cls.dtype, cls.op, cls.has_inverse
+
+
+def modulus_of(ops) -> int:
+    """The modulus of a mod-add monoid (0 for the others), validated."""
+    base = unwrap(ops)
+    name = getattr(base, "name", "")
+    if not (isinstance(name, str) and name.startswith("mod-add:")):
+        return 0
+    m = getattr(base, "modulus", None)
+    if m is None:
+        try:
+            m = int(name.split(":", 1)[1])
+        except ValueError:
+            raise ConfigurationError(f"bad mod-add modulus in {name!r}") from None
+    m = int(m)
+    if not 2 <= m <= MOD_ADD_MAX_MODULUS:
+        raise ConfigurationError(f"mod-add modulus must be in [2, {MOD_ADD_MAX_MODULUS}], got {m}")
+    return m

@@ -6,6 +6,8 @@ this module                    reference (pkg/src/exsum)
 bdbs_included(t, box)          included.py:124-129
 bdbs_excluded(t, box)          excluded.py:88-90 (+ _complement :72-75)
 box_complement_excluded(t,box) excluded.py:129-159
+sat_included(t, box)           included.py:98-121 (+ sat_build :37-42)
+sat_excluded(t, box)           excluded.py:83-85
 bdbs_1d(ops, values, k)        scan.py:53-58
 windowed_sum_axis(ops,v,k,ax)  scan.py:61-102 (in place on ``v``)
 ALGORITHMS / AlgorithmInfo     bench.py:45-100 (the plug-in registry)
@@ -34,25 +36,28 @@ import numpy as np
 
 from . import _native
 from .errors import ConfigurationError, UsageError
-from .monoid import device_operator
+from .monoid import device_operator, modulus_of
 from .tensor import Tensor, is_torch, normalize_box, np_dtype_of
 
 _DT_NAME = {np.dtype(np.float32): "float32", np.dtype(np.float64): "float64",
             np.dtype(np.int64): "int64"}
 
 
+_NEEDS_INVERSE = ("bdbsc", "sat", "satc")  # bench.py:60-76 needs_inverse
+
+
 def _prepare(t, box, route):
     dtype, op, has_inverse = device_operator(t.ops)
-    if route == "bdbsc" and not has_inverse:
+    if route in _NEEDS_INVERSE and not has_inverse:
         raise ConfigurationError(
-            f"algorithm 'bdbsc' requires an invertible monoid, but {t.ops.name!r} has no inverse"
+            f"algorithm {route!r} requires an invertible monoid, but {t.ops.name!r} has no inverse"
         )
     data = t.data
     ext = tuple(int(v) for v in data.shape)
     k = normalize_box(ext, box)
     if np_dtype_of(data) != dtype:
         raise UsageError(f"dtype {np_dtype_of(data)} does not match monoid {t.ops.name}")
-    return _DT_NAME[dtype], op, ext, k
+    return _DT_NAME[dtype], op, ext, k, modulus_of(t.ops)
 
 
 def _rewrap(t, out):
@@ -62,8 +67,9 @@ def _rewrap(t, out):
         return Tensor(t.ops, out)
 
 
-def run_device(route: str, x, dtype: str, op: str, ext, k, out=None):
-    """Run ``route`` on a CUDA torch tensor; returns the output tensor."""
+def run_device(route: str, x, dtype: str, op: str, ext, k, out=None, modulus: int = 0):
+    """Run ``route`` on a CUDA torch tensor; returns the output tensor.
+    ``modulus``: m of a ``mod-add:<m>`` operator (op == "mod-add")."""
     import torch
 
     if not x.is_cuda:
@@ -72,22 +78,19 @@ def run_device(route: str, x, dtype: str, op: str, ext, k, out=None):
     if out is None:
         out = torch.empty_like(x)
     L = _native.load()
-    ws_bytes = _native.workspace_bytes(route, dtype, op, ext, k)
+    ws_bytes = _native.workspace_bytes(route, dtype, op, ext, k, modulus)
     with torch.cuda.device(x.device):
         ws = torch.empty(max(ws_bytes, 1), dtype=torch.uint8, device=x.device)
         stream = torch.cuda.current_stream(x.device).cuda_stream
-        fn = {
-            "bdbs": L.exsum_bdbs_included,
-            "bdbsc": L.exsum_bdbsc_excluded,
-            "box-complement": L.exsum_box_complement_excluded,
-        }[route]
-        _native.check(fn(x.data_ptr(), out.data_ptr(), _native.DTYPE[dtype], _native.OP[op],
-                         len(ext), _native.i64_array(ext), _native.i64_array(k),
-                         ws.data_ptr(), ws_bytes, stream))
+        _native.check(L.exsum_route(_native.ROUTE[route], x.data_ptr(), out.data_ptr(),
+                                    _native.DTYPE[dtype], _native.OP[op], int(modulus), len(ext),
+                                    _native.i64_array(ext), _native.i64_array(k), ws.data_ptr(),
+                                    ws_bytes, stream))
     return out
 
 
-def run_host(route: str, a: np.ndarray, dtype: str, op: str, ext, k, out=None) -> np.ndarray:
+def run_host(route: str, a: np.ndarray, dtype: str, op: str, ext, k, out=None,
+             modulus: int = 0) -> np.ndarray:
     """Run ``route`` on a host array through exsum_run_host (H2D, compute, D2H).
 
     ``out`` (optional) receives the result; pass page-locked buffers (e.g. a
@@ -98,23 +101,23 @@ def run_host(route: str, a: np.ndarray, dtype: str, op: str, ext, k, out=None) -
     elif out.shape != a.shape or out.dtype != a.dtype or not out.flags.c_contiguous:
         raise UsageError("out must be a C-contiguous array of the input's shape and dtype")
     L = _native.load()
-    _native.check(L.exsum_run_host(_native.ROUTE[route], a.ctypes.data, out.ctypes.data,
-                                   _native.DTYPE[dtype], _native.OP[op], len(ext),
-                                   _native.i64_array(ext), _native.i64_array(k)))
+    _native.check(L.exsum_route_host(_native.ROUTE[route], a.ctypes.data, out.ctypes.data,
+                                     _native.DTYPE[dtype], _native.OP[op], int(modulus), len(ext),
+                                     _native.i64_array(ext), _native.i64_array(k)))
     return out
 
 
 def _route(route, t, box):
-    dtype, op, ext, k = _prepare(t, box, route)
+    dtype, op, ext, k, m = _prepare(t, box, route)
     data = t.data
     if is_torch(data):
         if data.is_cuda:
-            return _rewrap(t, run_device(route, data, dtype, op, ext, k))
-        out = run_host(route, data.numpy(), dtype, op, ext, k)
+            return _rewrap(t, run_device(route, data, dtype, op, ext, k, modulus=m))
+        out = run_host(route, data.numpy(), dtype, op, ext, k, modulus=m)
         import torch
 
         return _rewrap(t, torch.from_numpy(out))
-    return _rewrap(t, run_host(route, np.asarray(data), dtype, op, ext, k))
+    return _rewrap(t, run_host(route, np.asarray(data), dtype, op, ext, k, modulus=m))
 
 
 def bdbs_included(t, box):
@@ -132,12 +135,23 @@ def box_complement_excluded(t, box):
     return _route("box-complement", t, box)
 
 
+def sat_included(t, box):
+    """Included sum through a running-sum table and 2^d corner queries
+    (needs an invertible monoid)."""
+    return _route("sat", t, box)
+
+
+def sat_excluded(t, box):
+    """Total minus the table-based included sum (needs an invertible monoid)."""
+    return _route("satc", t, box)
+
+
 def bdbs_1d(ops, values, k):
     """Windowed sums of a 1-D sequence: out[x] = fold(values[x : x+k])."""
     dtype, op, _ = device_operator(ops)
     arr = np.array(values, dtype=dtype).reshape(-1)
     (kk,) = normalize_box(arr.shape, (k,))
-    return run_host("bdbs", arr, _DT_NAME[dtype], op, arr.shape, (kk,))
+    return run_host("bdbs", arr, _DT_NAME[dtype], op, arr.shape, (kk,), modulus=modulus_of(ops))
 
 
 def windowed_sum_axis(ops, view, k, axis):
@@ -188,7 +202,9 @@ class AlgorithmInfo:
 ALGORITHMS = {
     info.name: info
     for info in (
+        AlgorithmInfo("sat", sat_included, "included", True),
         AlgorithmInfo("bdbs", bdbs_included, "included", False),
+        AlgorithmInfo("satc", sat_excluded, "excluded", True),
         AlgorithmInfo("bdbsc", bdbs_excluded, "excluded", True),
         AlgorithmInfo("box-complement", box_complement_excluded, "excluded", False),
     )
@@ -220,7 +236,7 @@ def register_with_reference(bench_module) -> None:
     """Swap the reference's registry entries for the B200 routes.
 
     ``bench_module`` is the reference's ``exsum.bench``; afterwards
-    ``exsum run --algo bdbs|bdbsc|box-complement`` executes on the GPU
+    ``exsum run --algo sat|bdbs|satc|bdbsc|box-complement`` executes on the GPU
     (the monkeypatch precedent is test_bench.py:243-245).
     """
     ref_info = bench_module.AlgorithmInfo

@@ -273,6 +273,8 @@ class ShardedRunner:
         dtype, op, has_inverse = device_operator(ops)
         if route == "bdbsc" and not has_inverse:
             raise ConfigurationError(f"algorithm 'bdbsc' requires an invertible monoid")
+        if op == "mod-add":
+            raise ConfigurationError("the sharded path covers add and max; run mod-add on one GPU")
         self.ext = tuple(int(v) for v in ext)
         if len(self.ext) < 2 and route == "box-complement":
             raise ConfigurationError("sharded box-complement needs d >= 2")

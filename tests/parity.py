@@ -13,6 +13,11 @@ Exactness contract (north star):
       - box-complement: S(x) = box_complement(|A|)(x) + included(|A|)(x)
         (all terms are partial sums of |A| over subsets of the array), and
         D = sum_i(n_i + 2 k_i) + 16 (full-axis scans are the longest chains).
+      - sat / satc: every table entry is a prefix sum bounded by
+        sum(|A|) and the query folds 2^d of them, so S(x) = 2^d * sum(|A|)
+        (+ sum(|A|) for satc's total) and D = sum_i(n_i) + 2^d + 8.  Where the
+        scans run unsegmented the float tables are bit-identical to the
+        reference's (numpy's sequential accumulate), and so is sat itself.
     The float64 oracle's own error is D_ref * 2^-53 * S, negligible next to
     float32's u = 2^-24; for float64 data both sides count.
 """
@@ -29,6 +34,8 @@ def depth(route, ext, k):
         return sum(2 * kk for kk in k) + 4
     if route == "bdbsc":
         return sum(2 * kk for kk in k) + 8
+    if route in ("sat", "satc"):
+        return sum(ext) + 2 ** len(ext) + 8
     return sum(n + 2 * kk for n, kk in zip(ext, k)) + 16
 
 
@@ -42,6 +49,8 @@ def float_tolerance(route, a, k, oracle_mod):
     D = depth(route, ext, k)
     if route == "bdbsc":
         S = np.full(ext, a64.sum())
+    elif route in ("sat", "satc"):
+        S = np.full(ext, (2 ** len(ext) + (route == "satc")) * a64.sum())
     elif route == "box-complement":
         S = oracle_mod.box_complement_excluded(a64, k) + oracle_mod.bdbs_included(a64, k)
     else:

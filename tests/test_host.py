@@ -25,7 +25,7 @@ def test_library_exports_every_header_symbol():
     for name in names:
         assert hasattr(L, name), name
     assert set(names) == set(_native.EXPORTS)
-    assert L.exsum_abi_version() == 1
+    assert L.exsum_abi_version() == 2
 
 
 def test_library_is_sm100a():
@@ -64,18 +64,36 @@ def test_validation_happens_before_any_device_work():
     with pytest.raises(ex.ConfigurationError):
         ex.bdbs_excluded(tm, (2, 2))
     with pytest.raises(ex.ConfigurationError):
-        ex.resolve_monoid("mod-add:7")
+        ex.resolve_monoid("mod-add:1")
+    for route in (ex.sat_included, ex.sat_excluded):
+        with pytest.raises(ex.ConfigurationError):
+            route(tm, (2, 2))
+        with pytest.raises(ex.UsageError):
+            route(t, (2, 2, 2))
 
 
 def test_unsupported_monoid_is_configuration_error():
     class Weird:
-        name = "mod-add:11"
+        name = "xor-i64"
         dtype = np.dtype(np.int64)
         identity = 0
 
     t = ex.Tensor(Weird(), np.zeros((3,), dtype=np.int64))
     with pytest.raises(ex.ConfigurationError):
         ex.bdbs_included(t, (2,))
+
+    class RefMod:  # duck-typed like the reference's ModAddOps: modulus from the name
+        name = "mod-add:11"
+        dtype = np.dtype(np.int64)
+        identity = 0
+        has_inverse = True
+
+    from paper_2106_00124_b200.monoid import modulus_of
+
+    assert modulus_of(RefMod()) == 11
+    RefMod.name = "mod-add:1"
+    with pytest.raises(ex.ConfigurationError):
+        ex.bdbs_included(ex.Tensor(RefMod(), np.zeros((3,), dtype=np.int64)), (2,))
 
 
 def test_reference_style_monoids_and_instrumentation_unwrap():
@@ -97,6 +115,15 @@ def test_reference_style_monoids_and_instrumentation_unwrap():
     assert device_operator(Instrumented(RefAdd())) == (np.dtype(np.int64), "add", True)
     assert device_operator(ex.IntMaxOps()) == (np.dtype(np.int64), "max", False)
     assert device_operator(ex.Float32AddOps())[0] == np.dtype(np.float32)
+    assert device_operator(ex.ModAddOps(97)) == (np.dtype(np.int64), "mod-add", True)
+    assert device_operator(ex.resolve_monoid("mod-add:13"))[1] == "mod-add"
+    for bad in ("mod-add:1", "mod-add:x", "mod-add:", "sum"):
+        with pytest.raises(ex.ConfigurationError):
+            ex.resolve_monoid(bad)
+    with pytest.raises(ex.ConfigurationError):
+        ex.ModAddOps(2**31 + 1)
+    assert ex.ModAddOps(2**31).combine(2**31 - 1, 1) == 0
+    assert ex.ModAddOps(5).subtract(1, 3) == 3
 
 
 def test_no_cpu_fallback_without_gpu():
@@ -125,6 +152,18 @@ def test_c_abi_validation_codes():
     # device entry points refuse aliasing and null pointers before touching CUDA
     assert L.exsum_bdbs_included(None, None, 0, 0, 2, ext, box, None, 0, None) == 1
     assert L.exsum_bdbs_included(16, 16, 0, 0, 2, ext, box, None, 0, None) == 1
+    # sat / satc need an inverse; mod-add needs int64 and 2 <= m <= 2^31
+    rw = L.exsum_route_workspace_bytes
+    assert rw(3, 2, 1, 0, 2, ext, box, ctypes.byref(out)) == 2  # sat + max
+    assert b"'sat' requires an invertible" in L.exsum_last_error()
+    assert rw(4, 2, 1, 0, 2, ext, box, ctypes.byref(out)) == 2  # satc + max
+    assert rw(5, 2, 0, 0, 2, ext, box, ctypes.byref(out)) == 2  # no route 5
+    assert rw(3, 2, 0, 0, 2, ext, box, ctypes.byref(out)) == 0  # sat add-i64
+    for m, want in ((1, 2), (2, 0), (2**31, 0), (2**31 + 1, 2)):
+        assert rw(2, 2, 2, m, 2, ext, box, ctypes.byref(out)) == want, m
+    assert rw(0, 0, 2, 7, 2, ext, box, ctypes.byref(out)) == 2  # mod-add on float32
+    assert L.exsum_workspace_bytes(0, 2, 2, 2, ext, box, ctypes.byref(out)) == 2  # no modulus
+    assert L.exsum_route(0, None, None, 2, 2, 7, 2, ext, box, None, 0, None) == 1
 
 
 def test_workspace_sizes():
@@ -135,10 +174,24 @@ def test_workspace_sizes():
     # box-complement: W buffer + per-level reductions (<= N + small)
     ws = _native.workspace_bytes("box-complement", "float32", "add", (1024,) * 3, (16,) * 3)
     assert 4 * n <= ws <= 4 * n + 256 * 2**20  # W buffer + row partials + per-level reductions
+    # sat: the running-sum table; satc adds the reduction partials
+    assert _native.workspace_bytes("sat", "float32", "add", (1024,) * 3, (16,) * 3) == 4 * n
+    assert 4 * n < _native.workspace_bytes("satc", "float32", "add", (1024,) * 3, (16,) * 3) \
+        <= 4 * n + 2**20
+    # mod-add: canonical residues + the int64 route's own workspace
+    m = _native.workspace_bytes("bdbs", "int64", "mod-add", (256,) * 3, (8,) * 3, 97)
+    assert 2 * 8 * 256**3 <= m <= 2 * 8 * 256**3 + 2**20
+    # a long 1-D axis is scanned in segments (carry buffer, a few KB)
+    seg = _native.workspace_bytes("sat", "float64", "add", (1 << 22,), (5,))
+    assert 8 << 22 < seg < (8 << 22) + 2**20
 
 
 def test_registry_mirrors_reference():
-    assert set(ex.ALGORITHMS) == {"bdbs", "bdbsc", "box-complement"}
+    assert set(ex.ALGORITHMS) == {"sat", "bdbs", "satc", "bdbsc", "box-complement"}
+    for name in ("sat", "satc"):
+        with pytest.raises(ex.ConfigurationError):
+            ex.check_algorithm_config(ex.resolve_algorithm(name), ex.IntMaxOps())
+        ex.check_algorithm_config(ex.resolve_algorithm(name), ex.ModAddOps(7))
     info = ex.resolve_algorithm("bdbsc")
     assert info.needs_inverse and info.kind == "excluded"
     with pytest.raises(ex.ConfigurationError):
@@ -165,11 +218,13 @@ def test_register_with_reference_registry():
 
     fb = FakeBench()
     fb.AlgorithmInfo = AlgorithmInfo
-    fb.ALGORITHMS = {"bdbs": None, "sat": "untouched"}
+    fb.ALGORITHMS = {"bdbs": None, "naive-inc": "untouched"}
     ex.register_with_reference(fb)
     assert fb.ALGORITHMS["bdbs"].fn is ex.bdbs_included
     assert fb.ALGORITHMS["box-complement"].fn is ex.box_complement_excluded
-    assert fb.ALGORITHMS["sat"] == "untouched"
+    assert fb.ALGORITHMS["sat"].fn is ex.sat_included and fb.ALGORITHMS["sat"].needs_inverse
+    assert fb.ALGORITHMS["satc"].fn is ex.sat_excluded
+    assert fb.ALGORITHMS["naive-inc"] == "untouched"
 
 
 def test_pad_and_crop():
