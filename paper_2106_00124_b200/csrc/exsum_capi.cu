@@ -395,7 +395,8 @@ int scan_view(int dtype, const void* src, void* dst, int64_t outer, int64_t n, i
     nseg = (n + L - 1) / L;
   }
   if (live) {
-    ProfScope ps("sat_scan", 2.0 * (double)(outer * n * inner) * es, st);
+    ProfScope ps(inner == 1 ? "sat_scan_rows" : "sat_scan_strided",
+                 2.0 * (double)(outer * n * inner) * es, st);
     *launches += launch_scan(dtype, src, dst, outer, n, inner, L, nseg, st);
   }
   if (nseg > 1) {

@@ -41,54 +41,71 @@ namespace exsum {
 // 32 items per warp, one per lane, staged through a padded 32x33 tile.
 template <class T, int WARPS>
 __global__ void __launch_bounds__(WARPS * 32)
-k_scan_rows(const T* in, T* out, int64_t rows, int64_t n, int64_t L,
-            int64_t nseg) {
+k_scan_rows(const T* in, T* out, int64_t rows, int64_t n, int64_t L, int64_t nseg) {
   constexpr int W = 32;
   constexpr int STRIDE = W + 1;
   __shared__ T smem[WARPS][32 * STRIDE];
+  __shared__ int64_t sbase[WARPS][32], slen[WARPS][32];
   const int lane = threadIdx.x & 31;
-  T* sm = smem[threadIdx.x >> 5];
+  const int wid = threadIdx.x >> 5;
+  T* sm = smem[wid];
   const int64_t warp = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
   const int64_t nwarps = ((int64_t)gridDim.x * blockDim.x) >> 5;
   const int64_t items = rows * nseg;
   const int64_t groups = (items + 31) / 32;
   for (int64_t g = warp; g < groups; g += nwarps) {
     const int64_t i0 = g * 32;
-    const int ni = items - i0 >= 32 ? 32 : (int)(items - i0);
     int64_t mybase = 0, mylen = 0;
-    if (lane < ni) {
+    if (i0 + lane < items) {
       const int64_t it = i0 + lane;
       const int64_t row = it / nseg, seg = it - row * nseg;
       mybase = row * n + seg * L;
       mylen = n - seg * L < L ? n - seg * L : L;
     }
+    __syncwarp();
+    sbase[wid][lane] = mybase;
+    slen[wid][lane] = mylen;
     int64_t maxlen = mylen;
 #pragma unroll
     for (int o = 16; o >= 1; o >>= 1) {
       const int64_t v = __shfl_xor_sync(0xffffffffu, maxlen, o);
       maxlen = v > maxlen ? v : maxlen;
     }
+    __syncwarp();
     T acc = T(0);
     for (int64_t xo = 0; xo < maxlen; xo += W) {
-      for (int r = 0; r < ni; ++r) {
-        const int64_t b = __shfl_sync(0xffffffffu, mybase, r);
-        const int64_t l = __shfl_sync(0xffffffffu, mylen, r);
-        if (xo + lane < l) sm[r * STRIDE + lane] = ld1(in + b + xo + lane);
+      // 32 independent loads in flight, then the transpose into the tile
+      T v[32];
+#pragma unroll
+      for (int r = 0; r < 32; ++r) {
+        const int64_t l = slen[wid][r];
+        v[r] = xo + lane < l ? ld1(in + sbase[wid][r] + xo + lane) : T(0);
       }
+#pragma unroll
+      for (int r = 0; r < 32; ++r) sm[r * STRIDE + lane] = v[r];
       __syncwarp();
-      if (lane < ni) {
+      if (mylen > xo) {
         const int w = mylen - xo < W ? (int)(mylen - xo) : W;
-        for (int x = 0; x < w; ++x) {
-          const T v = sm[lane * STRIDE + x];
-          acc = (xo == 0 && x == 0) ? v : OpAdd::apply(acc, v);  // numpy: out[0] = a[0]
-          sm[lane * STRIDE + x] = acc;
+        if (w == W) {
+#pragma unroll
+          for (int x = 0; x < W; ++x) {
+            const T t = sm[lane * STRIDE + x];
+            acc = (xo == 0 && x == 0) ? t : OpAdd::apply(acc, t);  // numpy: out[0] = a[0]
+            sm[lane * STRIDE + x] = acc;
+          }
+        } else {
+          for (int x = 0; x < w; ++x) {
+            const T t = sm[lane * STRIDE + x];
+            acc = (xo == 0 && x == 0) ? t : OpAdd::apply(acc, t);
+            sm[lane * STRIDE + x] = acc;
+          }
         }
       }
       __syncwarp();
-      for (int r = 0; r < ni; ++r) {
-        const int64_t b = __shfl_sync(0xffffffffu, mybase, r);
-        const int64_t l = __shfl_sync(0xffffffffu, mylen, r);
-        if (xo + lane < l) st1(out + b + xo + lane, sm[r * STRIDE + lane]);
+#pragma unroll
+      for (int r = 0; r < 32; ++r) {
+        const int64_t l = slen[wid][r];
+        if (xo + lane < l) st1(out + sbase[wid][r] + xo + lane, sm[r * STRIDE + lane]);
       }
       __syncwarp();
     }
@@ -289,6 +306,300 @@ k_sat_query(const T* __restrict__ S, T* __restrict__ out, QShape q, int64_t N,
   }
 }
 
+// Row form of the query for d >= 2 (DH = d-1 leading axes, compile time).
+// A group of G lanes (G = the last extent rounded up to a power of two, <= 32)
+// owns one output row x' = (x_0..x_{d-2}); the 2^DH source rows of S for the
+// leading corner patterns are fixed for the whole row, so the per-element
+// work is two shifted loads (hi = min(x+k-1, n-1), lo = x-1) per source row
+// in the reference's product order (last axis fastest).  Rows are visited
+// with axis 0 in stride-k0 order (x0 = r + j*k0, j fastest): output planes
+// x0 and x0+k0 share the S plane x0+k0-1, so each S plane is fetched from
+// HBM about once and re-read from L2.
+template <class T, int DH>
+__global__ void __launch_bounds__(256)
+k_sat_query_rows(const T* __restrict__ S, T* __restrict__ out, QShape q, int64_t rows, int G,
+                 const typename AccOf<T>::type* __restrict__ total, int mode, FastMod fm) {
+  constexpr int NP = 1 << DH;
+  const int64_t n = q.ext[DH];
+  const int64_t kl = q.k[DH];
+  const int lane = threadIdx.x & 31;
+  const int slot = lane / G, sub = lane % G, slots = 32 / G;
+  const int64_t gwarp = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  const int64_t nwarps = ((int64_t)gridDim.x * blockDim.x) >> 5;
+  const int64_t n0 = q.ext[0], k0 = q.k[0];
+  const int64_t per0 = rows / n0;  // rows per axis-0 plane
+  T tot = T(0);
+  if (mode == QUERY_COMPLEMENT) tot = (T)(*total);
+  i64 tmod = 0;
+  if constexpr (std::is_same<T, i64>::value) {
+    if (mode == QUERY_MOD_COMPLEMENT) tmod = floor_mod((i64)(*total), fm);
+  }
+  for (int64_t rb = gwarp * slots; rb < rows; rb += nwarps * slots) {
+    const int64_t ri = rb + slot;
+    if (ri >= rows) continue;
+    // permuted axis-0 order: plane index p -> x0 = (p % m) * k0 + p / m
+    const int64_t p = ri / per0, rest = ri - p * per0;
+    const int64_t m = (n0 + k0 - 1) / k0;
+    const int64_t r0 = p / m, j0 = p - r0 * m;
+    int64_t x0 = j0 * k0 + r0;
+    int64_t hi_off[DH], lo_off[DH];
+    unsigned lo_ok = 0;
+    // the permutation is a bijection only when n0 % k0 == 0; otherwise fall
+    // back to the identity order
+    if (n0 % k0 != 0) x0 = p;
+    {
+      int64_t r = rest;
+#pragma unroll
+      for (int j = DH - 1; j >= 0; --j) {
+        int64_t xj;
+        if (j == 0) {
+          xj = x0;
+        } else {
+          xj = r % q.ext[j];
+          r /= q.ext[j];
+        }
+        const int64_t hi = xj + q.k[j] - 1 < q.ext[j] - 1 ? xj + q.k[j] - 1 : q.ext[j] - 1;
+        hi_off[j] = hi * q.str[j];
+        lo_off[j] = (xj - 1) * q.str[j];
+        if (xj > 0) lo_ok |= 1u << j;
+      }
+    }
+    int64_t obase = 0;
+    {
+      int64_t r = rest;
+#pragma unroll
+      for (int j = DH - 1; j >= 1; --j) {
+        obase += (r % q.ext[j]) * q.str[j];
+        r /= q.ext[j];
+      }
+      obase += x0 * q.str[0];
+    }
+    // the 2^DH source rows of this output row and which of them exist
+    const T* src[NP];
+    unsigned vmask = 0;
+    int par_mask = 0;
+#pragma unroll
+    for (int pp = 0; pp < NP; ++pp) {
+      int64_t base = 0;
+      unsigned need = 0;
+      int par = 0;
+#pragma unroll
+      for (int j = 0; j < DH; ++j) {
+        if ((pp >> (DH - 1 - j)) & 1) {
+          base += lo_off[j];
+          need |= 1u << j;
+          par ^= 1;
+        } else {
+          base += hi_off[j];
+        }
+      }
+      src[pp] = S + ((need & ~lo_ok) == 0 ? base : 0);  // invalid: any readable row
+      if ((need & ~lo_ok) == 0) vmask |= 1u << pp;
+      par_mask |= par << pp;
+    }
+    T* dst = out + obase;
+    const int nn = (int)n, kk = (int)kl;
+    // one output element: unconditional loads (identity terms come from a
+    // select, so signed zeros follow the reference's arithmetic exactly)
+    auto element = [&](int x) -> T {
+      const int hi = x + kk - 1 < nn - 1 ? x + kk - 1 : nn - 1;
+      const int lo = x > 0 ? x - 1 : 0;
+      T acc = T(0);
+#pragma unroll
+      for (int pp = 0; pp < NP; ++pp) {
+        const bool valid = (vmask >> pp) & 1;
+        const bool par = (par_mask >> pp) & 1;
+        const T h = __ldg(src[pp] + hi);
+        const T l = __ldg(src[pp] + lo);
+        const T vh = valid ? h : T(0);
+        const T vl = (valid && x > 0) ? l : T(0);
+        if (pp == 0) {
+          acc = vh;  // the all-high corner is copied (included.py:116-117)
+        } else {
+          acc = par ? OpAdd::inverse<T>(acc, vh) : OpAdd::apply(acc, vh);
+        }
+        acc = par ? OpAdd::apply(acc, vl) : OpAdd::inverse<T>(acc, vl);
+      }
+      if (mode == QUERY_COMPLEMENT) {
+        acc = OpAdd::inverse<T>(tot, acc);
+      } else if constexpr (std::is_same<T, i64>::value) {
+        if (mode == QUERY_MOD) {
+          acc = floor_mod(acc, fm);
+        } else if (mode == QUERY_MOD_COMPLEMENT) {
+          acc = floor_mod(OpAdd::inverse<T>(tmod, acc), fm);
+        }
+      }
+      return acc;
+    };
+    constexpr int XU = 4;  // x values per thread per step: XU * 2^(DH+1) loads in flight
+    int xb = sub;
+    for (; xb + (XU - 1) * G < nn; xb += XU * G) {
+      T r[XU];
+#pragma unroll
+      for (int u = 0; u < XU; ++u) r[u] = element(xb + u * G);
+#pragma unroll
+      for (int u = 0; u < XU; ++u) st1(dst + xb + u * G, r[u]);
+    }
+    for (; xb < nn; xb += G) st1(dst + xb, element(xb));
+  }
+}
+
+// Chained form of the staged query (d >= 2, long rows).  The last leading
+// axis c = d-2 is walked in steps of k_c: for output rows x_c = r + j k_c the
+// high corner of step j (row min(x_c + k_c - 1, n_c - 1)) is exactly the low
+// corner (row x_c' - 1) of step j+1, so every step stages only the 2^(d-2)
+// new high rows (one per pattern of the other leading axes) and reuses the
+// previous step's rows from shared memory -- half the L2->SM traffic of a
+// row-at-a-time form.  A 4-slot cp.async ring keeps two steps of prefetch in
+// flight (Little's law: ~64 KB per SM at HBM latency).  A work item (chain) is (the other leading coordinates, r); chains
+// are ordered so that CTAs running together share S planes in L2.
+template <class T, int DH>
+__global__ void __launch_bounds__(256)
+k_sat_query_chain(const T* __restrict__ S, T* __restrict__ out, QShape q, int64_t chains,
+                  const typename AccOf<T>::type* __restrict__ total, int mode, FastMod fm) {
+  constexpr int NQ = 1 << (DH - 1);  // patterns of the other leading axes
+  constexpr int C = DH - 1;          // chain axis
+  constexpr int VE = 16 / sizeof(T);
+  extern __shared__ __align__(16) unsigned char smem_raw[];
+  T* buf = reinterpret_cast<T*>(smem_raw);
+  const int n = (int)q.ext[DH];
+  const int kl = (int)q.k[DH];
+  const int pitch = n + VE;
+  const int slot_elems = NQ * pitch;
+  const int tid = threadIdx.x;
+  const int64_t nc = q.ext[C], kc = q.k[C];
+  const int64_t strc = q.str[C];
+  T tot = T(0);
+  if (mode == QUERY_COMPLEMENT) tot = (T)(*total);
+  i64 tmod = 0;
+  if constexpr (std::is_same<T, i64>::value) {
+    if (mode == QUERY_MOD_COMPLEMENT) tmod = floor_mod((i64)(*total), fm);
+  }
+  for (int i = tid; i < 4 * NQ * VE; i += 256) buf[(i / VE) * pitch + (i % VE)] = T(0);
+  __syncthreads();
+
+  for (int64_t ch = blockIdx.x; ch < chains; ch += gridDim.x) {
+    // chain -> (r, coordinates of axes 0..C-1); axis 0 in stride-k0 order
+    const int64_t r = ch % kc;
+    int64_t rest = ch / kc;
+    int64_t xs[DH > 1 ? DH - 1 : 1];
+    int64_t obase_lead = 0;
+    {
+#pragma unroll
+      for (int j = C - 1; j >= 0; --j) {
+        xs[j] = rest % q.ext[j];
+        rest /= q.ext[j];
+      }
+      if (C >= 1 && q.ext[0] % q.k[0] == 0) {  // permute axis 0: x0 = (p % m) k0 + p / m
+        const int64_t p = xs[0], m = q.ext[0] / q.k[0];
+        xs[0] = (p % m) * q.k[0] + p / m;
+      }
+#pragma unroll
+      for (int j = 0; j < C; ++j) obase_lead += xs[j] * q.str[j];
+    }
+    // per pattern q of axes 0..C-1: row offset (without the chain axis), validity, parity
+    int64_t qoff[NQ];
+    unsigned qvalid = 0;
+    int qpar = 0;
+#pragma unroll
+    for (int qq = 0; qq < NQ; ++qq) {
+      int64_t base = 0;
+      bool ok = true;
+      int par = 0;
+#pragma unroll
+      for (int j = 0; j < C; ++j) {
+        const bool lo = (qq >> (C - 1 - j)) & 1;
+        const int64_t xj = xs[j];
+        if (lo) {
+          base += (xj - 1) * q.str[j];
+          ok = ok && xj > 0;
+          par ^= 1;
+        } else {
+          const int64_t hi = xj + q.k[j] - 1 < q.ext[j] - 1 ? xj + q.k[j] - 1 : q.ext[j] - 1;
+          base += hi * q.str[j];
+        }
+      }
+      qoff[qq] = base;
+      if (ok) qvalid |= 1u << qq;
+      qpar |= par << qq;
+    }
+    // stage the 2^(d-2) rows at chain-axis row cr (cr < 0: identity rows)
+    auto stage = [&](int slot, int64_t cr) {
+      T* b = buf + (size_t)slot * slot_elems + VE;
+#pragma unroll
+      for (int qq = 0; qq < NQ; ++qq) {
+        T* row = b + qq * pitch;
+        if (((qvalid >> qq) & 1) && cr >= 0) {
+          const T* g = S + qoff[qq] + cr * strc;
+          for (int c = tid * VE; c < n; c += 256 * VE) cp_async16(row + c, g + c);
+        } else {
+          for (int c = tid; c < n; c += 256) row[c] = T(0);
+        }
+      }
+      cp_async_commit();
+    };
+    const int64_t steps = (nc - r + kc - 1) / kc;
+    auto hi_row = [&](int64_t j) {
+      const int64_t xc = r + j * kc;
+      return xc + kc - 1 < nc - 1 ? xc + kc - 1 : nc - 1;
+    };
+    // ring of RING slots: step j reads slots j % RING (low) and (j+1) % RING
+    // (high); the high rows of steps j+1 .. j+DEPTH are in flight
+    constexpr int RING = 4, DEPTH = RING - 2;
+    stage(0, r - 1);      // low rows of step 0
+    stage(1, hi_row(0));  // high rows of step 0
+#pragma unroll
+    for (int d = 1; d <= DEPTH; ++d) {
+      if (d < steps) stage(d + 1, hi_row(d));
+      else cp_async_commit();  // empty group keeps the wait counts uniform
+    }
+    for (int64_t j = 0; j < steps; ++j) {
+      const int lo_slot = (int)(j % RING), hi_slot = (int)((j + 1) % RING);
+      cp_async_wait<DEPTH>();  // groups up to step j's high rows have landed
+      __syncthreads();
+      const int64_t xc = r + j * kc;
+      const T* lob = buf + (size_t)lo_slot * slot_elems;
+      const T* hib = buf + (size_t)hi_slot * slot_elems;
+      T* dst = out + obase_lead + xc * strc;
+      for (int x = tid; x < n; x += 256) {
+        const int hi = VE + (x + kl - 1 < n - 1 ? x + kl - 1 : n - 1);
+        const int lo = VE - 1 + x;  // x - 1; the zero pad for x = 0
+        T acc = T(0);
+#pragma unroll
+        for (int pp = 0; pp < 2 * NQ; ++pp) {
+          const int qq = pp >> 1;
+          const bool clo = pp & 1;  // chain axis takes its low corner
+          const bool par = (((qpar >> qq) & 1) ^ (int)clo) != 0;
+          const T* rb = (clo ? lob : hib) + qq * pitch;
+          const T vh = rb[hi];
+          const T vl = rb[lo];
+          if (pp == 0) {
+            acc = vh;  // the all-high corner is copied (included.py:116-117)
+          } else {
+            acc = par ? OpAdd::inverse<T>(acc, vh) : OpAdd::apply(acc, vh);
+          }
+          acc = par ? OpAdd::apply(acc, vl) : OpAdd::inverse<T>(acc, vl);
+        }
+        if (mode == QUERY_COMPLEMENT) {
+          acc = OpAdd::inverse<T>(tot, acc);
+        } else if constexpr (std::is_same<T, i64>::value) {
+          if (mode == QUERY_MOD) {
+            acc = floor_mod(acc, fm);
+          } else if (mode == QUERY_MOD_COMPLEMENT) {
+            acc = floor_mod(OpAdd::inverse<T>(tmod, acc), fm);
+          }
+        }
+        st1(dst + x, acc);
+      }
+      __syncthreads();  // step j's low slot is refilled next, with step j+DEPTH+1's rows
+      if (j + DEPTH + 1 < steps) stage((int)((j + DEPTH + 2) % RING), hi_row(j + DEPTH + 1));
+      else cp_async_commit();
+    }
+    cp_async_wait<0>();
+    __syncthreads();
+  }
+}
+
 // ---------------------------------------------------------------- launchers --
 
 namespace {
@@ -312,14 +623,17 @@ int go_scan(const T* in, T* out, int64_t outer, int64_t n, int64_t inner, int64_
   }
   constexpr int VE = 16 / sizeof(T);
   const bool vec = inner % VE == 0 && ((uintptr_t)in % 16) == 0 && ((uintptr_t)out % 16) == 0;
-  if (vec) {
+  const int64_t want = (int64_t)num_sms() * 1024;
+  if (vec && outer * (inner / VE) * nseg >= want) {
     const int64_t work = outer * (inner / VE) * nseg;
     k_scan_strided<T, VE, 8><<<(unsigned)grid_for(work, 256, 8), 256, 0, s>>>(in, out, outer, n,
                                                                              inner, L, nseg);
   } else {
+    // few lines: one element per thread (VE-fold more threads) and 16 rows
+    // of loads in flight to cover the latency of the sequential walk
     const int64_t work = outer * inner * nseg;
-    k_scan_strided<T, 1, 8><<<(unsigned)grid_for(work, 256, 8), 256, 0, s>>>(in, out, outer, n,
-                                                                           inner, L, nseg);
+    k_scan_strided<T, 1, 16><<<(unsigned)grid_for(work, 256, 8), 256, 0, s>>>(in, out, outer, n,
+                                                                            inner, L, nseg);
   }
   return 1;
 }
@@ -329,6 +643,50 @@ int go_query(const T* S, T* out, const QShape& q, int64_t N, const void* total, 
              const FastMod& fm, cudaStream_t s) {
   typedef typename AccOf<T>::type Acc;
   const Acc* tot = (const Acc*)total;
+  constexpr int VE = 16 / sizeof(T);
+  if (q.d >= 2 && q.d <= 6 && q.ext[q.d - 1] >= 512 && q.ext[q.d - 1] % VE == 0 &&
+      ((uintptr_t)S % 16) == 0) {
+    const int64_t n = q.ext[q.d - 1];
+    const int NQ = 1 << (q.d - 2);
+    const size_t smem = (size_t)4 * NQ * (n + VE) * sizeof(T);
+    if (smem <= 96 * 1024) {
+      const int64_t chains = N / n / q.ext[q.d - 2] * q.k[q.d - 2];
+      const int per_sm = smem <= 50 * 1024 ? 4 : smem <= 64 * 1024 ? 3 : 2;
+      const int64_t cap = (int64_t)num_sms() * per_sm;
+      const unsigned gr = (unsigned)(chains < cap ? chains : cap);
+#define EXSUM_CHAIN(DH)                                                                        \
+  {                                                                                            \
+    auto kfn = k_sat_query_chain<T, DH>;                                                       \
+    ensure_smem((const void*)kfn, smem);                                                       \
+    kfn<<<gr, 256, smem, s>>>(S, out, q, chains, tot, mode, fm);                               \
+  }
+      switch (q.d) {
+        case 2: EXSUM_CHAIN(1) break;
+        case 3: EXSUM_CHAIN(2) break;
+        case 4: EXSUM_CHAIN(3) break;
+        case 5: EXSUM_CHAIN(4) break;
+        case 6: EXSUM_CHAIN(5) break;
+      }
+#undef EXSUM_CHAIN
+      return 1;
+    }
+  }
+  if (q.d >= 2 && q.d <= 6 && q.ext[q.d - 1] < (1LL << 30)) {
+    const int64_t n = q.ext[q.d - 1];
+    const int64_t rows = N / n;
+    int G = 1;  // lanes per row: each handles 4 x values per step (XU)
+    while (G < 32 && 4 * G < n) G *= 2;
+    const int64_t warps = (rows + (32 / G) - 1) / (32 / G);
+    const unsigned gr = (unsigned)grid_for(warps * 32, 256, 8);
+    switch (q.d) {
+      case 2: k_sat_query_rows<T, 1><<<gr, 256, 0, s>>>(S, out, q, rows, G, tot, mode, fm); break;
+      case 3: k_sat_query_rows<T, 2><<<gr, 256, 0, s>>>(S, out, q, rows, G, tot, mode, fm); break;
+      case 4: k_sat_query_rows<T, 3><<<gr, 256, 0, s>>>(S, out, q, rows, G, tot, mode, fm); break;
+      case 5: k_sat_query_rows<T, 4><<<gr, 256, 0, s>>>(S, out, q, rows, G, tot, mode, fm); break;
+      case 6: k_sat_query_rows<T, 5><<<gr, 256, 0, s>>>(S, out, q, rows, G, tot, mode, fm); break;
+    }
+    return 1;
+  }
   const unsigned g = (unsigned)grid_for(N, 256, 8);
   switch (q.d) {
     case 1: k_sat_query<T, 1><<<g, 256, 0, s>>>(S, out, q, N, tot, mode, fm); break;

@@ -30,6 +30,16 @@ CASES = {
            ["bdbs", "bdbsc"]),
     "c5bc": ((512, 512, 512), "float64", [(2, 2, 2), (8, 8, 8), (16, 16, 16)], ["box-complement"]),
     "c4bc": ((1024, 1024, 1024), "float32", [(4, 4, 4), (8, 8, 8), (16, 16, 16)], ["box-complement"]),
+    # sat / satc and the mod-add monoid
+    "c4sat": ((1024, 1024, 1024), "float32", [(16, 16, 16)], ["sat", "satc"]),
+    "c1sat": ((1024, 1024), "float64", [(32, 32)], ["sat", "satc"]),
+    "c3sat": ((256, 256, 256), "float32", [(4, 4, 4)], ["sat", "sat-i64"]),
+    "c3csat": ((64, 64, 64, 64), "float32", [(4,) * 4], ["sat"]),
+    "c3esat": ((16,) * 6, "float32", [(4,) * 6], ["sat"]),
+    "c5sat": ((512, 512, 512), "float64", [(8, 8, 8)], ["sat", "satc"]),
+    "c2mod": ((256, 256, 256), "int64", [(8, 8, 8)],
+              ["bdbs:mod-add:1000003", "bdbsc:mod-add:1000003", "box-complement:mod-add:1000003",
+               "sat:mod-add:1000003", "bdbs"]),
 }
 
 
@@ -61,12 +71,14 @@ def main():
                     if xi is None:
                         xi = torch.randint(-2**20, 2**20, ext, generator=g, device=dev)
                     x = xi
-                    ops = ex.IntMaxOps() if op == "max" else ex.IntAddOps()
+                    ops = (ex.IntMaxOps() if op == "max" else ex.resolve_monoid(op)
+                           if op.startswith("mod-add:") else ex.IntAddOps())
                 else:
                     x = xf
                     ops = ex.Float32AddOps() if dtype == "float32" else ex.FloatAddOps()
                 fn = {"bdbs": ex.bdbs_included, "bdbsc": ex.bdbs_excluded,
-                      "box-complement": ex.box_complement_excluded}[route]
+                      "box-complement": ex.box_complement_excluded, "sat": ex.sat_included,
+                      "satc": ex.sat_excluded}[route]
                 t = ex.Tensor(ops, x)
                 for _ in range(2):
                     fn(t, box)

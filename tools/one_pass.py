@@ -35,7 +35,8 @@ def main():
     if args.route:
         ops = ex.resolve_monoid({"float32": "add-f32", "float64": "add-f64"}.get(args.dtype, "max-i64" if args.op == "max" else "add-i64"))
         fn = {"bdbs": ex.bdbs_included, "bdbsc": ex.bdbs_excluded,
-              "box-complement": ex.box_complement_excluded}[args.route]
+              "box-complement": ex.box_complement_excluded, "sat": ex.sat_included,
+              "satc": ex.sat_excluded}[args.route]
         t = ex.Tensor(ops, x)
         for _ in range(args.reps):
             fn(t, (args.k,) * len(shape))
