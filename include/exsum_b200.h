@@ -54,6 +54,9 @@ extern "C" {
 #define EXSUM_ROUTE_BOX_COMPLEMENT 2 /* "box-complement" excluded.py:129-159 */
 #define EXSUM_ROUTE_SAT 3            /* "sat"            included.py:98-121  */
 #define EXSUM_ROUTE_SATC 4           /* "satc"           excluded.py:83-85   */
+#define EXSUM_ROUTE_CORNERS 5        /* "corners"        excluded.py:200-225 (2-D, 3-D) */
+#define EXSUM_ROUTE_CORNERS_SPINE 6  /* "corners-spine"  excluded.py:228-262 (2-D, 3-D);
+                                        same values as "corners" bit for bit */
 
 #define EXSUM_OK 0
 #define EXSUM_EUSAGE 1
@@ -77,9 +80,10 @@ int exsum_workspace_bytes(int route, int dtype, int op, int d, const int64_t *ex
 /* Any route (EXSUM_ROUTE_*) with any operator, including mod-add:<m>
  * (`modulus` is ignored for the other operators).  Replaces the registry slot
  * `fn(t, box)` of every bench.ALGORITHMS entry on this path (bench.py:60-76):
- * "bdbs", "bdbsc", "box-complement", "sat" (included.py:98-121) and "satc"
- * (excluded.py:83-85).  bdbsc / sat / satc need an invertible operator
- * (add, mod-add); max returns EXSUM_ECONFIG like bench.check_algorithm_config. */
+ * "bdbs", "bdbsc", "box-complement", "sat" (included.py:98-121), "satc"
+ * (excluded.py:83-85), "corners" and "corners-spine" (excluded.py:191-262).
+ * bdbsc / sat / satc need an invertible operator (add, mod-add); max returns
+ * EXSUM_ECONFIG like bench.check_algorithm_config; corners need d in {2, 3}. */
 int exsum_route(int route, const void *in, void *out, int dtype, int op, int64_t modulus, int d,
                 const int64_t *ext, const int64_t *box, void *ws, size_t ws_bytes, void *stream);
 int exsum_route_workspace_bytes(int route, int dtype, int op, int64_t modulus, int d,

@@ -25,6 +25,7 @@
  *
  *   - sat_included / sat_excluded included.py:37-121, excluded.py:83-85
  *   - mod-add:<m> monoid           monoid.py:235-286 (op code 2, oracle_set_modulus)
+ *   - corners / corners-spine      excluded.py:41-66, 191-292 (2-D, 3-D)
  *
  * dtype codes: 0 = float32, 1 = float64, 2 = int64.  op codes: 0 = add, 1 = max,
  * 2 = mod-add.
@@ -323,6 +324,84 @@ DEFINE_ORACLE(i64_mod, int64_t, mod_add, i64_add, floor_mod, 0)
         return ORC_OK;                                                                         \
     }
 
+/*
+ * Corner decompositions (excluded.py:41-66, 191-292): for every pattern in
+ * sorted order ("PP" < "PS" < ...), a copy of A accumulated along axes
+ * 0..d-1 in order -- forward for P, reversed for S (ops.accumulate) -- and
+ * its contribution combined into the identity-filled output: along each
+ * axis a prefix letter reads its scan at T-1 (clamped to n-1; nothing when
+ * T-1 < 0) and a suffix letter at T (nothing when T >= n), with T = x (near
+ * face) or x + k (far face) per the pattern's rule (CORNER_RULES,
+ * excluded.py:45-62).  corners_excluded and corners_spine_excluded produce the
+ * same scans and the same accumulation order, so one restatement serves both.
+ */
+static const char *const CORNER_KINDS2[4] = {"NF", "FF", "NN", "FN"};         /* PP PS SP SS */
+static const char *const CORNER_KINDS3[8] = {"FNF", "FFF", "NNF", "NFF",
+                                            "FNN", "FFN", "NNN", "NFN"};      /* PPP..SSS */
+
+#define DEFINE_CORNERS(SFX, T, C, ACC, FIN, IDENT)                                             \
+    static void line_scan_##SFX(T *s, int64_t outer, int64_t n, int64_t inner, int rev) {     \
+        _Pragma("omp parallel for schedule(static)")                                           \
+        for (int64_t l = 0; l < outer * inner; ++l) {                                          \
+            T *line = s + (l / inner) * n * inner + (l % inner);                               \
+            if (!rev) {                                                                        \
+                for (int64_t x = 1; x < n; ++x)                                                \
+                    line[x * inner] = ACC(line[(x - 1) * inner], line[x * inner]);             \
+            } else {                                                                           \
+                for (int64_t x = n - 2; x >= 0; --x)                                           \
+                    line[x * inner] = ACC(line[(x + 1) * inner], line[x * inner]);             \
+            }                                                                                  \
+            for (int64_t x = 0; x < n; ++x) line[x * inner] = FIN(line[x * inner]);            \
+        }                                                                                      \
+    }                                                                                          \
+    static int corners_##SFX(const T *in, T *out, int d, const int64_t *ext, const int64_t *k) { \
+        if (d != 2 && d != 3) return ORC_CONFIG;                                               \
+        int64_t N = prod_range(ext, 0, d);                                                     \
+        T *sc = (T *)malloc(sizeof(T) * (size_t)N);                                            \
+        if (!sc) return ORC_USAGE;                                                             \
+        for (int64_t i = 0; i < N; ++i) out[i] = (T)(IDENT);                                   \
+        int64_t str[3];                                                                        \
+        str[d - 1] = 1;                                                                        \
+        for (int j = d - 2; j >= 0; --j) str[j] = str[j + 1] * ext[j + 1];                     \
+        for (int p = 0; p < (1 << d); ++p) {                                                   \
+            const char *kinds = d == 2 ? CORNER_KINDS2[p] : CORNER_KINDS3[p];                  \
+            memcpy(sc, in, sizeof(T) * (size_t)N);                                             \
+            for (int a = 0; a < d; ++a) {                                                      \
+                int suffix = (p >> (d - 1 - a)) & 1;                                           \
+                line_scan_##SFX(sc, prod_range(ext, 0, a), ext[a], prod_range(ext, a + 1, d), suffix); \
+            }                                                                                  \
+            _Pragma("omp parallel for schedule(static)")                                       \
+            for (int64_t f = 0; f < N; ++f) {                                                  \
+                int64_t r = f, idx = 0;                                                        \
+                int ok = 1;                                                                    \
+                for (int a = d - 1; a >= 0; --a) {                                             \
+                    int64_t x = r % ext[a];                                                    \
+                    r /= ext[a];                                                               \
+                    int suffix = (p >> (d - 1 - a)) & 1;                                       \
+                    int64_t t = kinds[a] == 'N' ? x : x + k[a];                                \
+                    int64_t src;                                                               \
+                    if (!suffix) {                                                             \
+                        if (t - 1 < 0) { ok = 0; break; }                                      \
+                        src = t - 1 < ext[a] - 1 ? t - 1 : ext[a] - 1;                         \
+                    } else {                                                                   \
+                        if (t >= ext[a]) { ok = 0; break; }                                    \
+                        src = t;                                                               \
+                    }                                                                          \
+                    idx += src * str[a];                                                       \
+                }                                                                              \
+                if (ok) out[f] = C(out[f], sc[idx]);                                           \
+            }                                                                                  \
+        }                                                                                      \
+        free(sc);                                                                              \
+        return ORC_OK;                                                                         \
+    }
+
+DEFINE_CORNERS(f32_add, float, C_FADD, C_FADD, C_NOFIN, 0.0f)
+DEFINE_CORNERS(f64_add, double, C_FADD, C_FADD, C_NOFIN, 0.0)
+DEFINE_CORNERS(i64_add, int64_t, C_IADD, C_IADD, C_NOFIN, 0)
+DEFINE_CORNERS(i64_max, int64_t, C_MAX, C_MAX, C_NOFIN, INT64_MIN)
+DEFINE_CORNERS(i64_mod, int64_t, mod_add, i64_add, floor_mod, 0)
+
 DEFINE_SAT(f32_add, float, C_FADD, C_FSUB, C_FADD, C_NOFIN, 0.0f)
 DEFINE_SAT(f64_add, double, C_FADD, C_FSUB, C_FADD, C_NOFIN, 0.0)
 DEFINE_SAT(i64_add, int64_t, C_IADD, C_ISUB, C_IADD, C_NOFIN, 0)
@@ -421,6 +500,21 @@ int oracle_box_complement_excluded(const void *in, void *out, int dtype, int op,
     if (dtype == 2 && op == 0) return box_complement_i64_add(in, out, d, ext, k);
     if (dtype == 2 && op == 1) return box_complement_i64_max(in, out, d, ext, k);
     if (dtype == 2 && op == 2) return box_complement_i64_mod(in, out, d, ext, k);
+    return ORC_CONFIG;
+}
+
+/* "corners" / "corners-spine" (excluded.py:191-292), 2-D and 3-D only. */
+int oracle_corners_excluded(const void *in, void *out, int dtype, int op, int d,
+                            const int64_t *ext, const int64_t *box, int nthreads) {
+    int64_t k[16];
+    int rc = normalize(d, ext, box, k);
+    if (rc) return rc;
+    set_threads(nthreads);
+    if (dtype == 0 && op == 0) return corners_f32_add(in, out, d, ext, k);
+    if (dtype == 1 && op == 0) return corners_f64_add(in, out, d, ext, k);
+    if (dtype == 2 && op == 0) return corners_i64_add(in, out, d, ext, k);
+    if (dtype == 2 && op == 1) return corners_i64_max(in, out, d, ext, k);
+    if (dtype == 2 && op == 2) return corners_i64_mod(in, out, d, ext, k);
     return ORC_CONFIG;
 }
 

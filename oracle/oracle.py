@@ -64,6 +64,7 @@ def lib():
             "oracle_box_complement_excluded",
             "oracle_sat_included",
             "oracle_satc_excluded",
+            "oracle_corners_excluded",
             "oracle_brute_included",
             "oracle_brute_excluded",
         ):
@@ -142,6 +143,10 @@ def sat_excluded(a, box, op="add", nthreads=0):
     return _run("oracle_satc_excluded", a, box, op, nthreads)
 
 
+def corners_excluded(a, box, op="add", nthreads=0):
+    return _run("oracle_corners_excluded", a, box, op, nthreads)
+
+
 def brute_included(a, box, op="add", nthreads=0):
     return _run("oracle_brute_included", a, box, op, nthreads)
 
@@ -156,6 +161,8 @@ ROUTES = {
     "box-complement": box_complement_excluded,
     "sat": sat_included,
     "satc": sat_excluded,
+    "corners": corners_excluded,
+    "corners-spine": corners_excluded,
 }
 
 

@@ -34,6 +34,8 @@ from .routes import (
     bdbs_included,
     box_complement_excluded,
     check_algorithm_config,
+    corners_excluded,
+    corners_spine_excluded,
     register_with_reference,
     resolve_algorithm,
     sat_excluded,
@@ -49,7 +51,8 @@ __all__ = [
     "Float32AddOps", "FloatAddOps", "IntAddOps", "IntMaxOps", "MONOID_CHOICES", "ModAddOps",
     "MonoidOps",
     "Tensor", "UsageError", "VerificationError", "bdbs_1d", "bdbs_excluded", "bdbs_included",
-    "box_complement_excluded", "check_algorithm_config", "crop_to", "normalize_box",
+    "box_complement_excluded", "check_algorithm_config", "corners_excluded",
+    "corners_spine_excluded", "crop_to", "normalize_box",
     "pad_to_box_multiple", "register_with_reference", "resolve_algorithm", "resolve_monoid",
     "sat_excluded", "sat_included",
     "validate_extents", "windowed_sum_axis",

@@ -22,7 +22,8 @@ LIB_PATH = os.environ.get("EXSUM_LIB") or os.path.join(
 
 DTYPE = {"float32": 0, "float64": 1, "int64": 2}
 OP = {"add": 0, "max": 1, "mod-add": 2}
-ROUTE = {"bdbs": 0, "bdbsc": 1, "box-complement": 2, "sat": 3, "satc": 4}
+ROUTE = {"bdbs": 0, "bdbsc": 1, "box-complement": 2, "sat": 3, "satc": 4, "corners": 5,
+         "corners-spine": 6}
 ABI_VERSION = 2
 
 EXPORTS = (

@@ -9,6 +9,8 @@
 //                                          axis first (see below)
 //   sat / satc      included.py:37-121,   running-sum table (d sequential
 //                   excluded.py:83-85     scans) + one 2^d-corner query (sat.cu)
+//   corners         excluded.py:191-292   2^d scanned copies (P/S per axis) and
+//                                          their corner contributions (2-D, 3-D)
 //   mod-add:<m>     monoid.py:235-286     any route: canonical residues, the
 //                                          exact int64 + route, a mod-m epilogue
 //
@@ -381,7 +383,7 @@ int route_box_complement(const Shape& s, int dtype, int op, const void* src, voi
 // axis is cut into segments: local scans, an (in-place, recursive) scan of
 // the segment totals, and a carry pass.
 int scan_view(int dtype, const void* src, void* dst, int64_t outer, int64_t n, int64_t inner,
-              Arena& ar, cudaStream_t st, int* launches) {
+              Arena& ar, cudaStream_t st, int* launches, int op = EXSUM_ADD, int rev = 0) {
   const size_t es = dtype_size(dtype);
   const bool live = ar.base != nullptr;
   const int64_t ve = (int64_t)(16 / es);
@@ -397,14 +399,15 @@ int scan_view(int dtype, const void* src, void* dst, int64_t outer, int64_t n, i
   if (live) {
     ProfScope ps(inner == 1 ? "sat_scan_rows" : "sat_scan_strided",
                  2.0 * (double)(outer * n * inner) * es, st);
-    *launches += launch_scan(dtype, src, dst, outer, n, inner, L, nseg, st);
+    *launches += launch_scan(dtype, op, src, dst, outer, n, inner, L, nseg, rev, st);
   }
   if (nseg > 1) {
     void* tot = ar.take((size_t)(outer * (nseg - 1) * inner) * es);
-    if (live) *launches += launch_seg_carry(dtype, dst, tot, outer, n, inner, L, nseg, 0, st);
-    int rc = scan_view(dtype, tot, tot, outer, nseg - 1, inner, ar, st, launches);
+    if (live) *launches += launch_seg_carry(dtype, op, dst, tot, outer, n, inner, L, nseg, rev, 0, st);
+    // totals are stored in (possibly reversed) line order: a forward scan
+    int rc = scan_view(dtype, tot, tot, outer, nseg - 1, inner, ar, st, launches, op, 0);
     if (rc) return rc;
-    if (live) *launches += launch_seg_carry(dtype, dst, tot, outer, n, inner, L, nseg, 1, st);
+    if (live) *launches += launch_seg_carry(dtype, op, dst, tot, outer, n, inner, L, nseg, rev, 1, st);
   }
   return EXSUM_OK;
 }
@@ -450,6 +453,55 @@ int route_sat(const Shape& s, int dtype, const void* in, void* out, Arena& ar, i
     }
     ProfScope ps("sat_query", 2.0 * (double)s.N * es, st);
     *launches += launch_sat_query(dtype, table, out, q, s.N, total, qmode, fm, st);
+  }
+  return EXSUM_OK;
+}
+
+// "corners" / "corners-spine" (excluded.py:191-292; 2-D and 3-D): for every
+// pattern in sorted order, a copy of A accumulated along axes 0..d-1 (P:
+// forward, S: reversed; sequential per line like numpy) and its contribution
+// combined into out.  The reference's two variants differ only in how many
+// scanned copies they keep (buffers / cache depth); they scan the same
+// tensors and accumulate in the same order, so one device route serves both
+// (its workspace is one scanned copy, the leaf-buffered form with c = 1).
+int route_corners(const Shape& s, int dtype, int op, const void* in, void* out, Arena& ar,
+                  cudaStream_t st, int* launches) {
+  // CORNER_RULES (excluded.py:45-62) in sorted pattern order, one bit per
+  // axis (bit a set: the threshold is the far face x_a + k_a)
+  static const int kFar2[4] = {0b01, 0b11, 0b00, 0b10};                    // PP PS SP SS
+  static const int kFar3[8] = {0b101, 0b111, 0b001, 0b011, 0b100, 0b110, 0b000, 0b010};
+  const size_t es = dtype_size(dtype);
+  const bool live = ar.base != nullptr;
+  const int d = s.d;
+  void* sc = ar.take((size_t)s.N * es);
+  CornerSpec cs;
+  cs.d = d;
+  int64_t stride = 1;
+  for (int a = d - 1; a >= 0; --a) {
+    cs.ext[a] = s.ext[a];
+    cs.k[a] = s.k[a];
+    cs.str[a] = stride;
+    stride *= s.ext[a];
+  }
+  for (int p = 0; p < (1 << d); ++p) {
+    const int far_msb = d == 2 ? kFar2[p] : kFar3[p];  // bit (d-1-a) <-> axis a
+    cs.suffix = 0;
+    cs.far = 0;
+    for (int a = 0; a < d; ++a) {
+      if ((p >> (d - 1 - a)) & 1) cs.suffix |= 1 << a;
+      if ((far_msb >> (d - 1 - a)) & 1) cs.far |= 1 << a;
+    }
+    const void* cur = in;
+    for (int a = 0; a < d; ++a) {
+      int rc = scan_view(dtype, cur, sc, prod(s.ext, 0, a), s.ext[a], prod(s.ext, a + 1, d), ar,
+                         st, launches, op, (cs.suffix >> a) & 1);
+      if (rc) return rc;
+      cur = sc;
+    }
+    if (live) {
+      ProfScope ps("corner_apply", (p == 0 ? 2.0 : 3.0) * (double)s.N * es, st);
+      *launches += launch_corner_apply(dtype, op, sc, out, cs, s.N, p == 0, st);
+    }
   }
   return EXSUM_OK;
 }
@@ -515,6 +567,10 @@ int route_modadd(int route, const Shape& s, int64_t modulus, const void* in, voi
     case EXSUM_ROUTE_BOX_COMPLEMENT:
       rc = route_box_complement(s, EXSUM_I64, EXSUM_ADD, canon, out, ar, st, launches);
       break;
+    case EXSUM_ROUTE_CORNERS:
+    case EXSUM_ROUTE_CORNERS_SPINE:
+      rc = route_corners(s, EXSUM_I64, EXSUM_ADD, canon, out, ar, st, launches);
+      break;
     default:
       rc = route_bdbs(s, EXSUM_I64, EXSUM_ADD, canon, out, ar, false, st, launches);
       break;
@@ -553,6 +609,9 @@ int dispatch(int route, const Shape& s, int dtype, int op, int64_t modulus, cons
       return route_sat(s, dtype, in, out, ar, QUERY_PLAIN, nullptr, fm, st, launches);
     case EXSUM_ROUTE_SATC:
       return route_sat(s, dtype, in, out, ar, QUERY_COMPLEMENT, nullptr, fm, st, launches);
+    case EXSUM_ROUTE_CORNERS:
+    case EXSUM_ROUTE_CORNERS_SPINE:
+      return route_corners(s, dtype, op, in, out, ar, st, launches);
   }
   return fail(EXSUM_ECONFIG, "unknown route");
 }
@@ -561,10 +620,15 @@ int validate(int route, int dtype, int op, int64_t modulus, int d, const int64_t
              const int64_t* box, Shape* s) {
   int rc = check_types(dtype, op, modulus);
   if (rc) return rc;
-  if (route < 0 || route > EXSUM_ROUTE_SATC) return fail(EXSUM_ECONFIG, "unknown route");
+  if (route < 0 || route > EXSUM_ROUTE_CORNERS_SPINE) return fail(EXSUM_ECONFIG, "unknown route");
+  // _corner_rules (excluded.py:191-197): rule tables exist for 2-D and 3-D only
+  if ((route == EXSUM_ROUTE_CORNERS || route == EXSUM_ROUTE_CORNERS_SPINE) && d != 2 && d != 3)
+    return fail(EXSUM_ECONFIG, "corner decomposition is only defined for 2-D and 3-D tensors, got " +
+                                   std::to_string(d) + "-D");
   // bench.check_algorithm_config (bench.py:88-100): bdbsc, sat and satc need
   // an inverse (bench.py:61-69, needs_inverse)
-  if (op == EXSUM_MAX && route != EXSUM_ROUTE_BDBS && route != EXSUM_ROUTE_BOX_COMPLEMENT) {
+  if (op == EXSUM_MAX &&
+      (route == EXSUM_ROUTE_BDBSC || route == EXSUM_ROUTE_SAT || route == EXSUM_ROUTE_SATC)) {
     const char* name = route == EXSUM_ROUTE_BDBSC ? "bdbsc" : route == EXSUM_ROUTE_SAT ? "sat" : "satc";
     return fail(EXSUM_ECONFIG, std::string("algorithm '") + name +
                                    "' requires an invertible monoid, but 'max-i64' has no inverse");

@@ -84,15 +84,26 @@ int launch_fused_pair(int dtype, int op, const void* in, void* out, int64_t oute
 
 // ---------------------------------------------- sat / satc / mod-add (sat.cu)
 
-// Inclusive running sum (np.add.accumulate) along the middle axis of
-// [outer, n, inner], restarted every L elements (nseg = ceil(n / L) segments;
+// Inclusive running fold (ops.accumulate: np.add / np.maximum .accumulate)
+// along the middle axis of [outer, n, inner] -- reversed (suffix) when rev --
+// restarted every L elements of the (possibly reversed) line (nseg segments;
 // nseg == 1: plain sequential scan).  in == out is allowed.
-int launch_scan(int dtype, const void* in, void* out, int64_t outer, int64_t n, int64_t inner,
-                int64_t L, int64_t nseg, cudaStream_t s);
+int launch_scan(int dtype, int op, const void* in, void* out, int64_t outer, int64_t n,
+                int64_t inner, int64_t L, int64_t nseg, int rev, cudaStream_t s);
 // Segmented scans: step 0 gathers the segment totals into tot[outer, nseg-1,
-// inner]; step 1 adds the scanned totals back as carries.
-int launch_seg_carry(int dtype, void* out, void* tot, int64_t outer, int64_t n, int64_t inner,
-                     int64_t L, int64_t nseg, int step, cudaStream_t s);
+// inner]; step 1 folds the scanned totals back in as carries.
+int launch_seg_carry(int dtype, int op, void* out, void* tot, int64_t outer, int64_t n,
+                     int64_t inner, int64_t L, int64_t nseg, int rev, int step, cudaStream_t s);
+
+// One corner pattern's contribution into out (first: out = identity (+) it).
+struct CornerSpec {
+  int d;
+  int64_t ext[3], k[3], str[3];
+  int suffix;  // bit a: axis a is a suffix (S) letter
+  int far;     // bit a: the threshold is the far face x + k
+};
+int launch_corner_apply(int dtype, int op, const void* sc, void* out, const CornerSpec& cs,
+                        int64_t N, int first, cudaStream_t s);
 
 #define EXSUM_QMAX 32
 struct QShape {

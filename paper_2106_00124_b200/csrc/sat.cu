@@ -39,9 +39,9 @@ namespace exsum {
 // Inclusive running sum along the contiguous axis of [rows, n], in segments
 // of L (nseg per row; nseg == 1: whole rows).  Work item = (row, segment);
 // 32 items per warp, one per lane, staged through a padded 32x33 tile.
-template <class T, int WARPS>
+template <class T, class Op, int WARPS>
 __global__ void __launch_bounds__(WARPS * 32)
-k_scan_rows(const T* in, T* out, int64_t rows, int64_t n, int64_t L, int64_t nseg) {
+k_scan_rows(const T* in, T* out, int64_t rows, int64_t n, int64_t L, int64_t nseg, int rev) {
   constexpr int W = 32;
   constexpr int STRIDE = W + 1;
   __shared__ T smem[WARPS][32 * STRIDE];
@@ -59,9 +59,11 @@ k_scan_rows(const T* in, T* out, int64_t rows, int64_t n, int64_t L, int64_t nse
     if (i0 + lane < items) {
       const int64_t it = i0 + lane;
       const int64_t row = it / nseg, seg = it - row * nseg;
-      mybase = row * n + seg * L;
+      // line position p = seg*L + x lives at row*n + p (or n-1-p reversed)
+      mybase = row * n + (rev ? n - 1 - seg * L : seg * L);
       mylen = n - seg * L < L ? n - seg * L : L;
     }
+    const int64_t dir = rev ? -1 : 1;
     __syncwarp();
     sbase[wid][lane] = mybase;
     slen[wid][lane] = mylen;
@@ -79,7 +81,7 @@ k_scan_rows(const T* in, T* out, int64_t rows, int64_t n, int64_t L, int64_t nse
 #pragma unroll
       for (int r = 0; r < 32; ++r) {
         const int64_t l = slen[wid][r];
-        v[r] = xo + lane < l ? ld1(in + sbase[wid][r] + xo + lane) : T(0);
+        v[r] = xo + lane < l ? ld1(in + sbase[wid][r] + dir * (xo + lane)) : T(0);
       }
 #pragma unroll
       for (int r = 0; r < 32; ++r) sm[r * STRIDE + lane] = v[r];
@@ -90,13 +92,13 @@ k_scan_rows(const T* in, T* out, int64_t rows, int64_t n, int64_t L, int64_t nse
 #pragma unroll
           for (int x = 0; x < W; ++x) {
             const T t = sm[lane * STRIDE + x];
-            acc = (xo == 0 && x == 0) ? t : OpAdd::apply(acc, t);  // numpy: out[0] = a[0]
+            acc = (xo == 0 && x == 0) ? t : Op::apply(acc, t);  // numpy: out[0] = a[0]
             sm[lane * STRIDE + x] = acc;
           }
         } else {
           for (int x = 0; x < w; ++x) {
             const T t = sm[lane * STRIDE + x];
-            acc = (xo == 0 && x == 0) ? t : OpAdd::apply(acc, t);
+            acc = (xo == 0 && x == 0) ? t : Op::apply(acc, t);
             sm[lane * STRIDE + x] = acc;
           }
         }
@@ -105,7 +107,7 @@ k_scan_rows(const T* in, T* out, int64_t rows, int64_t n, int64_t L, int64_t nse
 #pragma unroll
       for (int r = 0; r < 32; ++r) {
         const int64_t l = slen[wid][r];
-        if (xo + lane < l) st1(out + sbase[wid][r] + xo + lane, sm[r * STRIDE + lane]);
+        if (xo + lane < l) st1(out + sbase[wid][r] + dir * (xo + lane), sm[r * STRIDE + lane]);
       }
       __syncwarp();
     }
@@ -115,10 +117,10 @@ k_scan_rows(const T* in, T* out, int64_t rows, int64_t n, int64_t L, int64_t nse
 // Inclusive running sum along the middle axis of [outer, n, inner]; a thread
 // owns VE consecutive columns (one 16-byte vector when inner allows) of one
 // segment and walks it with U rows of loads in flight.  In place is allowed.
-template <class T, int VE, int U>
+template <class T, class Op, int VE, int U>
 __global__ void __launch_bounds__(256)
 k_scan_strided(const T* in, T* out, int64_t outer, int64_t n,
-               int64_t inner, int64_t L, int64_t nseg) {
+               int64_t inner, int64_t L, int64_t nseg, int rev) {
   typedef Vec<T, VE> VT;
   const int64_t cols = inner / VE;
   const int64_t items = outer * cols * nseg;
@@ -130,15 +132,18 @@ k_scan_strided(const T* in, T* out, int64_t outer, int64_t n,
     const int64_t seg = rest / outer;
     const int64_t xs = seg * L;
     const int64_t xe = xs + L < n ? xs + L : n;
-    const T* src = in + (o * n + xs) * inner + c * VE;
-    T* dst = out + (o * n + xs) * inner + c * VE;
+    // line position p lives at row p (or n-1-p reversed)
+    const int64_t step = rev ? -inner : inner;
+    const int64_t first = rev ? n - 1 - xs : xs;
+    const T* src = in + (o * n + first) * inner + c * VE;
+    T* dst = out + (o * n + first) * inner + c * VE;
     VT acc;
     for (int64_t x = 0; x < xe - xs; x += U) {
       const int cnt = xe - xs - x < U ? (int)(xe - xs - x) : U;
       VT buf[U];
 #pragma unroll
       for (int u = 0; u < U; ++u)
-        if (u < cnt) buf[u] = *reinterpret_cast<const VT*>(src + (x + u) * inner);
+        if (u < cnt) buf[u] = *reinterpret_cast<const VT*>(src + (x + u) * step);
 #pragma unroll
       for (int u = 0; u < U; ++u)
         if (u < cnt) {
@@ -146,9 +151,9 @@ k_scan_strided(const T* in, T* out, int64_t outer, int64_t n,
             acc = buf[0];
           } else {
 #pragma unroll
-            for (int j = 0; j < VE; ++j) acc.v[j] = OpAdd::apply(acc.v[j], buf[u].v[j]);
+            for (int j = 0; j < VE; ++j) acc.v[j] = Op::apply(acc.v[j], buf[u].v[j]);
           }
-          *reinterpret_cast<VT*>(dst + (x + u) * inner) = acc;
+          *reinterpret_cast<VT*>(dst + (x + u) * step) = acc;
         }
     }
   }
@@ -157,7 +162,7 @@ k_scan_strided(const T* in, T* out, int64_t outer, int64_t n,
 // Segmented scans, step 2: T[o, s, i] = out[o, (s+1) L - 1, i] for s < nseg-1.
 template <class T>
 __global__ void k_seg_gather(const T* __restrict__ out, T* __restrict__ tot, int64_t outer,
-                             int64_t n, int64_t inner, int64_t L, int64_t nseg) {
+                             int64_t n, int64_t inner, int64_t L, int64_t nseg, int rev) {
   const int64_t cnt = outer * (nseg - 1) * inner;
   for (int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; e < cnt;
        e += (int64_t)gridDim.x * blockDim.x) {
@@ -165,15 +170,16 @@ __global__ void k_seg_gather(const T* __restrict__ out, T* __restrict__ tot, int
     const int64_t rest = e / inner;
     const int64_t s = rest % (nseg - 1);
     const int64_t o = rest / (nseg - 1);
-    tot[e] = out[(o * n + (s + 1) * L - 1) * inner + i];
+    const int64_t pos = (s + 1) * L - 1;
+    tot[e] = out[(o * n + (rev ? n - 1 - pos : pos)) * inner + i];
   }
 }
 
 // Segmented scans, step 4: out[o, x, i] = Tscan[o, x/L - 1, i] (+) out[o, x, i]
 // for x >= L (Tscan: inclusive scan of the segment totals).
-template <class T>
+template <class T, class Op>
 __global__ void k_carry_add(T* __restrict__ out, const T* __restrict__ tscan, int64_t outer,
-                            int64_t n, int64_t inner, int64_t L, int64_t nseg) {
+                            int64_t n, int64_t inner, int64_t L, int64_t nseg, int rev) {
   const int64_t cnt = outer * (n - L) * inner;
   for (int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; e < cnt;
        e += (int64_t)gridDim.x * blockDim.x) {
@@ -182,8 +188,8 @@ __global__ void k_carry_add(T* __restrict__ out, const T* __restrict__ tscan, in
     const int64_t x = L + rest % (n - L);
     const int64_t o = rest / (n - L);
     const int64_t s = x / L;
-    T* p = out + (o * n + x) * inner + i;
-    *p = OpAdd::apply(tscan[(o * (nseg - 1) + s - 1) * inner + i], *p);
+    T* p = out + (o * n + (rev ? n - 1 - x : x)) * inner + i;
+    *p = Op::apply(tscan[(o * (nseg - 1) + s - 1) * inner + i], *p);
   }
 }
 
@@ -600,6 +606,44 @@ k_sat_query_chain(const T* __restrict__ S, T* __restrict__ out, QShape q, int64_
   }
 }
 
+// ------------------------------------------------------------- corners --
+
+// One corner pattern's contribution (excluded.py:218-234): along axis a the
+// scanned copy is read at T-1 clamped to n-1 (prefix letter; nothing when
+// T-1 < 0) or at T (suffix letter; nothing when T >= n), T = x (near face)
+// or x + k (far face).  first: out starts from the identity (Tensor.filled).
+template <class T, class Op>
+__global__ void k_corner_apply(const T* __restrict__ sc, T* __restrict__ out, CornerSpec cs,
+                               int64_t N, int first) {
+  for (int64_t f = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; f < N;
+       f += (int64_t)gridDim.x * blockDim.x) {
+    int64_t r = f, idx = 0;
+    bool ok = true;
+#pragma unroll
+    for (int a = 2; a >= 0; --a) {
+      if (a >= cs.d) continue;
+      const int64_t x = r % cs.ext[a];
+      r /= cs.ext[a];
+      const int64_t t = (cs.far >> a) & 1 ? x + cs.k[a] : x;
+      int64_t src;
+      if ((cs.suffix >> a) & 1) {
+        ok = ok && t < cs.ext[a];
+        src = t;
+      } else {
+        ok = ok && t >= 1;
+        src = t - 1 < cs.ext[a] - 1 ? t - 1 : cs.ext[a] - 1;
+      }
+      idx += src * cs.str[a];
+    }
+    if (first) {
+      const T id = Op::template identity<T>();
+      st1(out + f, ok ? Op::apply(id, sc[idx]) : id);
+    } else if (ok) {
+      out[f] = Op::apply(out[f], sc[idx]);
+    }
+  }
+}
+
 // ---------------------------------------------------------------- launchers --
 
 namespace {
@@ -611,14 +655,14 @@ int64_t grid_for(int64_t work, int threads, int per_sm) {
   return g < 1 ? 1 : g;
 }
 
-template <class T>
+template <class T, class Op>
 int go_scan(const T* in, T* out, int64_t outer, int64_t n, int64_t inner, int64_t L, int64_t nseg,
-            cudaStream_t s) {
+            int rev, cudaStream_t s) {
   if (inner == 1) {
     constexpr int WARPS = 4;
     const int64_t groups = (outer * nseg + 31) / 32;
-    k_scan_rows<T, WARPS><<<(unsigned)grid_for(groups * 32, WARPS * 32, 16), WARPS * 32, 0, s>>>(
-        in, out, outer, n, L, nseg);
+    k_scan_rows<T, Op, WARPS><<<(unsigned)grid_for(groups * 32, WARPS * 32, 16), WARPS * 32, 0,
+                                s>>>(in, out, outer, n, L, nseg, rev);
     return 1;
   }
   constexpr int VE = 16 / sizeof(T);
@@ -626,14 +670,14 @@ int go_scan(const T* in, T* out, int64_t outer, int64_t n, int64_t inner, int64_
   const int64_t want = (int64_t)num_sms() * 1024;
   if (vec && outer * (inner / VE) * nseg >= want) {
     const int64_t work = outer * (inner / VE) * nseg;
-    k_scan_strided<T, VE, 8><<<(unsigned)grid_for(work, 256, 8), 256, 0, s>>>(in, out, outer, n,
-                                                                             inner, L, nseg);
+    k_scan_strided<T, Op, VE, 8><<<(unsigned)grid_for(work, 256, 8), 256, 0, s>>>(
+        in, out, outer, n, inner, L, nseg, rev);
   } else {
     // few lines: one element per thread (VE-fold more threads) and 16 rows
     // of loads in flight to cover the latency of the sequential walk
     const int64_t work = outer * inner * nseg;
-    k_scan_strided<T, 1, 16><<<(unsigned)grid_for(work, 256, 8), 256, 0, s>>>(in, out, outer, n,
-                                                                            inner, L, nseg);
+    k_scan_strided<T, Op, 1, 16><<<(unsigned)grid_for(work, 256, 8), 256, 0, s>>>(
+        in, out, outer, n, inner, L, nseg, rev);
   }
   return 1;
 }
@@ -702,32 +746,56 @@ int go_query(const T* S, T* out, const QShape& q, int64_t N, const void* total, 
 
 }  // namespace
 
-int launch_scan(int dtype, const void* in, void* out, int64_t outer, int64_t n, int64_t inner,
-                int64_t L, int64_t nseg, cudaStream_t s) {
+int launch_scan(int dtype, int op, const void* in, void* out, int64_t outer, int64_t n,
+                int64_t inner, int64_t L, int64_t nseg, int rev, cudaStream_t s) {
+  if (op == 1) {
+    if (dtype != 2) return -1;
+    return go_scan<i64, OpMax>((const i64*)in, (i64*)out, outer, n, inner, L, nseg, rev, s);
+  }
   switch (dtype) {
-    case 0: return go_scan((const float*)in, (float*)out, outer, n, inner, L, nseg, s);
-    case 1: return go_scan((const double*)in, (double*)out, outer, n, inner, L, nseg, s);
-    case 2: return go_scan((const i64*)in, (i64*)out, outer, n, inner, L, nseg, s);
+    case 0: return go_scan<float, OpAdd>((const float*)in, (float*)out, outer, n, inner, L, nseg, rev, s);
+    case 1: return go_scan<double, OpAdd>((const double*)in, (double*)out, outer, n, inner, L, nseg, rev, s);
+    case 2: return go_scan<i64, OpAdd>((const i64*)in, (i64*)out, outer, n, inner, L, nseg, rev, s);
   }
   return -1;
 }
 
-int launch_seg_carry(int dtype, void* out, void* tot, int64_t outer, int64_t n, int64_t inner,
-                     int64_t L, int64_t nseg, int step, cudaStream_t s) {
+int launch_seg_carry(int dtype, int op, void* out, void* tot, int64_t outer, int64_t n,
+                     int64_t inner, int64_t L, int64_t nseg, int rev, int step, cudaStream_t s) {
   const int64_t work = step == 0 ? outer * (nseg - 1) * inner : outer * (n - L) * inner;
   const unsigned g = (unsigned)grid_for(work, 256, 8);
-#define EXSUM_SEG(T)                                                                          \
-  if (step == 0)                                                                              \
-    k_seg_gather<T><<<g, 256, 0, s>>>((const T*)out, (T*)tot, outer, n, inner, L, nseg);      \
-  else                                                                                        \
-    k_carry_add<T><<<g, 256, 0, s>>>((T*)out, (const T*)tot, outer, n, inner, L, nseg);       \
+#define EXSUM_SEG(T, OP)                                                                        \
+  if (step == 0)                                                                                \
+    k_seg_gather<T><<<g, 256, 0, s>>>((const T*)out, (T*)tot, outer, n, inner, L, nseg, rev);   \
+  else                                                                                          \
+    k_carry_add<T, OP><<<g, 256, 0, s>>>((T*)out, (const T*)tot, outer, n, inner, L, nseg, rev); \
   return 1;
+  if (op == 1) {
+    if (dtype != 2) return -1;
+    EXSUM_SEG(i64, OpMax)
+  }
   switch (dtype) {
-    case 0: { EXSUM_SEG(float) }
-    case 1: { EXSUM_SEG(double) }
-    case 2: { EXSUM_SEG(i64) }
+    case 0: { EXSUM_SEG(float, OpAdd) }
+    case 1: { EXSUM_SEG(double, OpAdd) }
+    case 2: { EXSUM_SEG(i64, OpAdd) }
   }
 #undef EXSUM_SEG
+  return -1;
+}
+
+int launch_corner_apply(int dtype, int op, const void* sc, void* out, const CornerSpec& cs,
+                        int64_t N, int first, cudaStream_t s) {
+  const unsigned g = (unsigned)grid_for(N, 256, 8);
+  if (op == 1) {
+    if (dtype != 2) return -1;
+    k_corner_apply<i64, OpMax><<<g, 256, 0, s>>>((const i64*)sc, (i64*)out, cs, N, first);
+    return 1;
+  }
+  switch (dtype) {
+    case 0: k_corner_apply<float, OpAdd><<<g, 256, 0, s>>>((const float*)sc, (float*)out, cs, N, first); return 1;
+    case 1: k_corner_apply<double, OpAdd><<<g, 256, 0, s>>>((const double*)sc, (double*)out, cs, N, first); return 1;
+    case 2: k_corner_apply<i64, OpAdd><<<g, 256, 0, s>>>((const i64*)sc, (i64*)out, cs, N, first); return 1;
+  }
   return -1;
 }
 

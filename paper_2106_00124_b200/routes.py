@@ -8,6 +8,8 @@ bdbs_excluded(t, box)          excluded.py:88-90 (+ _complement :72-75)
 box_complement_excluded(t,box) excluded.py:129-159
 sat_included(t, box)           included.py:98-121 (+ sat_build :37-42)
 sat_excluded(t, box)           excluded.py:83-85
+corners_excluded(t, box, c)    excluded.py:200-225 (2-D, 3-D)
+corners_spine_excluded(t,b,c)  excluded.py:228-262 (2-D, 3-D)
 bdbs_1d(ops, values, k)        scan.py:53-58
 windowed_sum_axis(ops,v,k,ax)  scan.py:61-102 (in place on ``v``)
 ALGORITHMS / AlgorithmInfo     bench.py:45-100 (the plug-in registry)
@@ -146,6 +148,33 @@ def sat_excluded(t, box):
     return _route("satc", t, box)
 
 
+def _corner_checks(t, box, c, label):
+    """_corner_rules (excluded.py:191-197) then normalize_box then the space
+    factor, in the reference's order."""
+    d = len(t.data.shape)
+    if d not in (2, 3):
+        raise ConfigurationError(
+            f"corner decomposition is only defined for 2-D and 3-D tensors, got {d}-D"
+        )
+    normalize_box(tuple(int(v) for v in t.data.shape), box)
+    if not isinstance(c, (int, np.integer)) or not 1 <= int(c) <= d:
+        raise UsageError(f"{label} must be in [1, {d}] for a {d}-D tensor, got {c}")
+
+
+def corners_excluded(t, box, buffers: int = 1):
+    """Strong excluded sum by the 2^d corner decomposition (any monoid, 2-D/3-D).
+    ``buffers`` is the reference's space factor; the GPU keeps one scanned
+    copy whatever its value (the values do not depend on it)."""
+    _corner_checks(t, box, buffers, "corners buffer count")
+    return _route("corners", t, box)
+
+
+def corners_spine_excluded(t, box, cache_depth: int = 1):
+    """Spine-cached corner decomposition (same values as corners_excluded)."""
+    _corner_checks(t, box, cache_depth, "cache depth")
+    return _route("corners-spine", t, box)
+
+
 def bdbs_1d(ops, values, k):
     """Windowed sums of a 1-D sequence: out[x] = fold(values[x : x+k])."""
     dtype, op, _ = device_operator(ops)
@@ -207,6 +236,9 @@ ALGORITHMS = {
         AlgorithmInfo("satc", sat_excluded, "excluded", True),
         AlgorithmInfo("bdbsc", bdbs_excluded, "excluded", True),
         AlgorithmInfo("box-complement", box_complement_excluded, "excluded", False),
+        AlgorithmInfo("corners", corners_excluded, "excluded", False, {2, 3}, "buffers"),
+        AlgorithmInfo("corners-spine", corners_spine_excluded, "excluded", False, {2, 3},
+                      "cache_depth"),
     )
 }
 
@@ -229,16 +261,21 @@ def check_algorithm_config(info: AlgorithmInfo, ops, d=None) -> None:
             f"but {getattr(ops, 'name', ops)!r} has no inverse"
         )
     if d is not None and info.dims is not None and d not in info.dims:
-        raise ConfigurationError(f"algorithm {info.name!r} does not support {d}-D tensors")
+        dims = ", ".join(str(v) for v in sorted(info.dims))
+        raise ConfigurationError(
+            f"algorithm {info.name!r} supports {dims}-D tensors only, got {d}-D"
+        )
 
 
 def register_with_reference(bench_module) -> None:
     """Swap the reference's registry entries for the B200 routes.
 
     ``bench_module`` is the reference's ``exsum.bench``; afterwards
-    ``exsum run --algo sat|bdbs|satc|bdbsc|box-complement`` executes on the GPU
+    ``exsum run --algo sat|bdbs|satc|bdbsc|box-complement|corners|corners-spine``
+    executes on the GPU
     (the monkeypatch precedent is test_bench.py:243-245).
     """
     ref_info = bench_module.AlgorithmInfo
     for name, info in ALGORITHMS.items():
-        bench_module.ALGORITHMS[name] = ref_info(name, info.fn, info.kind, info.needs_inverse)
+        bench_module.ALGORITHMS[name] = ref_info(name, info.fn, info.kind, info.needs_inverse,
+                                                 info.dims, info.cache_arg)

@@ -2,7 +2,7 @@
 
 Run in the build container (where /root/reference exists):
 
-    python tests/golden/make_golden.py [--only-ext]
+    python tests/golden/make_golden.py [--only-ext | --only-corners]
 
 It imports the unmodified reference package read-only from
 /root/reference/pkg/src (``exsum``), runs its public entry points
@@ -296,9 +296,72 @@ def make_ext():
     print("wrote ext.npz:", len(meta), "outputs")
 
 
+def make_corners():
+    """corners.npz: corners_excluded (every buffer count) and
+    corners_spine_excluded (every cache depth), excluded.py:191-292, on 2-D
+    and 3-D inputs for every monoid, through the reference."""
+    ex = _import_reference()
+    from exsum.excluded import corners_excluded, corners_spine_excluded
+
+    class AddF32(ex.FloatAddOps):
+        name = "add-f32"
+        dtype = np.dtype(np.float32)
+        identity = np.float32(0.0)
+
+    def mono(name):
+        return AddF32() if name == "add-f32" else ex.resolve_monoid(name)
+
+    out, meta = {}, []
+    rng = np.random.default_rng(191)
+    monos = ["add-i64", "max-i64", "add-f64", "add-f32", "mod-add:11", "mod-add:2147483648"]
+    ci = 0
+    for d, count in [(2, 24), (3, 24)]:
+        for _ in range(count):
+            ext = tuple(int(v) for v in rng.integers(1, 8 if d == 2 else 6, size=d))
+            box = tuple(int(rng.integers(1, n + 2)) for n in ext)
+            mname = monos[ci % len(monos)]
+            ops = mono(mname)
+            if ops.dtype.kind == "f":
+                arr = rng.random(ext).astype(ops.dtype)
+            elif mname.startswith("mod-add"):
+                arr = rng.integers(-3 * 11, 3 * 11, size=ext).astype(np.int64)
+            else:
+                arr = rng.integers(-100, 100, size=ext).astype(np.int64)
+            tag = f"k{ci}"
+            out[f"{tag}/in"] = arr
+            results = []
+            for c in range(1, d + 1):
+                results.append(corners_excluded(ex.Tensor(ops, arr.copy()), box, buffers=c).data)
+                results.append(corners_spine_excluded(ex.Tensor(ops, arr.copy()), box,
+                                                      cache_depth=c).data)
+            for r in results[1:]:  # every variant agrees bit for bit
+                assert r.tobytes() == results[0].tobytes()
+            out[f"{tag}/out"] = results[0].copy()
+            meta.append({"tag": tag, "mono": mname, "box": list(box), "ext": list(ext)})
+            ci += 1
+    r0 = np.random.default_rng(0)
+    for tag, arr, mname, box in [
+        ("c2like", r0.integers(-2**20, 2**20, size=(24, 20, 28), dtype=np.int64), "max-i64",
+         (8, 8, 8)),
+        ("c4like", r0.random((32, 24, 40), dtype=np.float32), "add-f32", (16, 16, 16)),
+        ("c1like", r0.random((96, 80)), "add-f64", (32, 32)),
+        ("c2add", r0.integers(-2**20, 2**20, size=(20, 18, 22), dtype=np.int64), "add-i64",
+         (4, 5, 3)),
+    ]:
+        out[f"{tag}/in"] = arr
+        out[f"{tag}/out"] = corners_excluded(ex.Tensor(mono(mname), arr.copy()), box).data.copy()
+        meta.append({"tag": tag, "mono": mname, "box": list(box), "ext": list(arr.shape)})
+    out["meta"] = np.frombuffer(json.dumps(meta).encode(), dtype=np.uint8)
+    np.savez_compressed(os.path.join(HERE, "corners.npz"), **out)
+    print("wrote corners.npz:", len(meta), "cases")
+
+
 if __name__ == "__main__":
     if "--only-ext" in sys.argv:
         make_ext()
+    elif "--only-corners" in sys.argv:
+        make_corners()
     else:
         make()
         make_ext()
+        make_corners()

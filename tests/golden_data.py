@@ -71,3 +71,15 @@ def ext_cases():
         m["out"] = z[m["key"]]
         m["in"] = z[m["in"]]
         yield m
+
+
+def corner_cases():
+    """Yield dicts (tag, mono, box, ext, 'in', 'out') for corners.npz
+    (corners_excluded / corners_spine_excluded, which agree bit for bit)."""
+    z = load("corners")
+    meta = json.loads(bytes(z["meta"]).decode())
+    for m in meta:
+        m = dict(m)
+        m["in"] = z[m["tag"] + "/in"]
+        m["out"] = z[m["tag"] + "/out"]
+        yield m

@@ -11,7 +11,7 @@ where the table scans run unsegmented, otherwise within tests/parity.py.
 import numpy as np
 import pytest
 
-from golden_data import ext_cases, mono_op
+from golden_data import corner_cases, ext_cases, mono_op
 from oracle import oracle as orc
 from parity import compare, float64_oracle
 
@@ -32,7 +32,8 @@ def ex():
 def _fn(ex, route):
     return {"bdbs": ex.bdbs_included, "bdbsc": ex.bdbs_excluded,
             "box-complement": ex.box_complement_excluded, "sat": ex.sat_included,
-            "satc": ex.sat_excluded}[route]
+            "satc": ex.sat_excluded, "corners": ex.corners_excluded,
+            "corners-spine": ex.corners_spine_excluded}[route]
 
 
 def _mono(ex, name):
@@ -173,3 +174,41 @@ def test_sat_workspace_and_launches(ex):
     ex.sat_included(t, (4, 4, 4))
     torch.cuda.synchronize()
     assert ex._native.total_launch_count() - before == 4  # 3 scans + 1 query
+
+
+def test_corners_golden_vectors(ex):
+    """corners / corners-spine (excluded.py:191-292) against the reference:
+    sequential scans and the reference's accumulation order, so floats too are
+    bit-exact."""
+    n = 0
+    for m in corner_cases():
+        for route in ("corners", "corners-spine"):
+            for device in (True, False):
+                got = _run(ex, route, m["mono"], m["in"], tuple(m["box"]), device)
+                assert _bits_equal(got, m["out"]), (m["tag"], route, device)
+        n += 1
+    assert n >= 50
+
+
+@pytest.mark.parametrize("mono", ["add-i64", "max-i64", "add-f64", "add-f32", "mod-add:97"])
+def test_corners_vs_oracle_and_box_complement(ex, mono):
+    rng = np.random.default_rng(7)
+    for shape, box in [((200, 150), (9, 30)), ((64, 48, 80), (4, 7, 16)), ((1, 300), (1, 5)),
+                       ((5000, 3), (100, 2)), ((3, 4, 5000), (2, 2, 64))]:
+        if mono.startswith("add-f"):
+            a = rng.random(shape).astype(np.float32 if mono == "add-f32" else np.float64)
+        else:
+            a = rng.integers(-2**20, 2**20, size=shape, dtype=np.int64)
+        got = _run(ex, "corners", mono, a, box)
+        want = orc.corners_excluded(a, box, mono_op(mono))
+        if a.dtype.kind == "f" and max(shape) < 4096:
+            assert _bits_equal(got, want), (mono, shape)  # unsegmented scans: exact
+        elif a.dtype.kind == "f":
+            k = tuple(min(b, e) for b, e in zip(box, shape))
+            ok, ratio, rel = compare("box-complement", got,
+                                     orc.corners_excluded(a.astype(np.float64), box), a, k, orc)
+            assert ok, (mono, shape, ratio)
+        else:
+            assert np.array_equal(got, want), (mono, shape)
+            # and the strong excluded sum is the same whichever decomposition
+            assert np.array_equal(got, _run(ex, "box-complement", mono, a, box))

@@ -88,14 +88,18 @@ def test_cli_configuration_errors_exit_2(capsys):
     assert cli.main(["sweep", "--algos", "bdbs", "--dims", "a:b"]) == 2
     err = capsys.readouterr().err
     assert "requires an invertible monoid" in err
+    # corners: 2-D / 3-D only (bench.check_algorithm_config dims), c in [1, d]
+    assert cli.main(["run", "--algo", "corners", "--extents", "4", "--box", "2"]) == 2
+    assert cli.main(["run", "--algo", "corners-spine", "--extents", "4,4,4,4", "--box", "2"]) == 2
+    assert cli.main(["run", "--algo", "corners", "--extents", "4,4", "--box", "2", "--c", "3"]) == 2
     with pytest.raises(SystemExit) as e:
-        cli.main(["run", "--algo", "corners", "--extents", "4", "--box", "2"])
+        cli.main(["run", "--algo", "naive-inc", "--extents", "4", "--box", "2"])
     assert e.value.code == 2
 
 
 @pytest.mark.gpu
 def test_run_benchmark_verifies_every_route():
-    for algo in ("bdbs", "bdbsc", "box-complement", "sat", "satc"):
+    for algo in ("bdbs", "bdbsc", "box-complement", "sat", "satc", "corners", "corners-spine"):
         for mono in ("add-i64", "add-f64", "add-f32", "mod-add:13", "max-i64"):
             if mono == "max-i64" and algo in ("bdbsc", "sat", "satc"):
                 continue

@@ -157,7 +157,11 @@ def test_c_abi_validation_codes():
     assert rw(3, 2, 1, 0, 2, ext, box, ctypes.byref(out)) == 2  # sat + max
     assert b"'sat' requires an invertible" in L.exsum_last_error()
     assert rw(4, 2, 1, 0, 2, ext, box, ctypes.byref(out)) == 2  # satc + max
-    assert rw(5, 2, 0, 0, 2, ext, box, ctypes.byref(out)) == 2  # no route 5
+    assert rw(7, 2, 0, 0, 2, ext, box, ctypes.byref(out)) == 2  # no route 7
+    assert rw(5, 2, 1, 0, 2, ext, box, ctypes.byref(out)) == 0  # corners, max, 2-D
+    one = _native.i64_array((4,))
+    assert rw(5, 2, 0, 0, 1, one, one, ctypes.byref(out)) == 2  # corners, 1-D
+    assert b"2-D and 3-D" in L.exsum_last_error(), L.exsum_last_error()
     assert rw(3, 2, 0, 0, 2, ext, box, ctypes.byref(out)) == 0  # sat add-i64
     for m, want in ((1, 2), (2, 0), (2**31, 0), (2**31 + 1, 2)):
         assert rw(2, 2, 2, m, 2, ext, box, ctypes.byref(out)) == want, m
@@ -187,7 +191,22 @@ def test_workspace_sizes():
 
 
 def test_registry_mirrors_reference():
-    assert set(ex.ALGORITHMS) == {"sat", "bdbs", "satc", "bdbsc", "box-complement"}
+    assert set(ex.ALGORITHMS) == {"sat", "bdbs", "satc", "bdbsc", "box-complement", "corners",
+                                  "corners-spine"}
+    assert ex.resolve_algorithm("corners").cache_arg == "buffers"
+    assert ex.resolve_algorithm("corners-spine").cache_arg == "cache_depth"
+    with pytest.raises(ex.ConfigurationError):
+        ex.check_algorithm_config(ex.resolve_algorithm("corners"), ex.IntAddOps(), 4)
+    t1 = ex.Tensor(ex.IntAddOps(), np.zeros(5, dtype=np.int64))
+    t2 = ex.Tensor(ex.IntAddOps(), np.zeros((3, 4), dtype=np.int64))
+    with pytest.raises(ex.ConfigurationError):
+        ex.corners_excluded(t1, (2,))
+    with pytest.raises(ex.UsageError):
+        ex.corners_excluded(t2, (2, 2), buffers=3)
+    with pytest.raises(ex.UsageError):
+        ex.corners_spine_excluded(t2, (2, 2), cache_depth=0)
+    with pytest.raises(ex.UsageError):
+        ex.corners_excluded(t2, (2,))
     for name in ("sat", "satc"):
         with pytest.raises(ex.ConfigurationError):
             ex.check_algorithm_config(ex.resolve_algorithm(name), ex.IntMaxOps())
@@ -198,7 +217,7 @@ def test_registry_mirrors_reference():
         ex.check_algorithm_config(info, ex.IntMaxOps())
     ex.check_algorithm_config(ex.resolve_algorithm("box-complement"), ex.IntMaxOps())
     with pytest.raises(ex.ConfigurationError):
-        ex.resolve_algorithm("corners")
+        ex.resolve_algorithm("naive-inc")  # not on the accelerated path
 
 
 def test_register_with_reference_registry():
@@ -225,6 +244,7 @@ def test_register_with_reference_registry():
     assert fb.ALGORITHMS["sat"].fn is ex.sat_included and fb.ALGORITHMS["sat"].needs_inverse
     assert fb.ALGORITHMS["satc"].fn is ex.sat_excluded
     assert fb.ALGORITHMS["naive-inc"] == "untouched"
+    assert fb.ALGORITHMS["corners"].cache_arg == "buffers" and fb.ALGORITHMS["corners"].dims == {2, 3}
 
 
 def test_pad_and_crop():

@@ -8,7 +8,8 @@ association -- and agree with the brute-force oracle restatement.
 import numpy as np
 import pytest
 
-from golden_data import MONO_OP, ext_cases, load, medium_cases, mono_op, small_cases
+from golden_data import (MONO_OP, corner_cases, ext_cases, load, medium_cases, mono_op,
+                         small_cases)
 from oracle import oracle as orc
 
 
@@ -117,3 +118,13 @@ def test_ext_sat_and_mod_add_bit_exact():
         assert np.array_equal(got.view(np.uint8), m["out"].view(np.uint8)), m["key"]
         n += 1
     assert n >= 1000
+
+
+def test_corners_bit_exact():
+    """corners / corners-spine (excluded.py:191-292) against the reference."""
+    n = 0
+    for m in corner_cases():
+        got = orc.corners_excluded(m["in"], tuple(m["box"]), mono_op(m["mono"]))
+        assert np.array_equal(got.view(np.uint8), m["out"].view(np.uint8)), m["tag"]
+        n += 1
+    assert n >= 50
