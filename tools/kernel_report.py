@@ -37,6 +37,8 @@ CASES = {
     "c3csat": ((64, 64, 64, 64), "float32", [(4,) * 4], ["sat"]),
     "c3esat": ((16,) * 6, "float32", [(4,) * 6], ["sat"]),
     "c5sat": ((512, 512, 512), "float64", [(8, 8, 8)], ["sat", "satc"]),
+    "c2corners": ((256, 256, 256), "int64", [(8, 8, 8)], ["corners:max", "box-complement:max"]),
+    "c1corners": ((1024, 1024), "float64", [(32, 32)], ["corners", "box-complement"]),
     "c2mod": ((256, 256, 256), "int64", [(8, 8, 8)],
               ["bdbs:mod-add:1000003", "bdbsc:mod-add:1000003", "box-complement:mod-add:1000003",
                "sat:mod-add:1000003", "bdbs"]),
@@ -78,7 +80,7 @@ def main():
                     ops = ex.Float32AddOps() if dtype == "float32" else ex.FloatAddOps()
                 fn = {"bdbs": ex.bdbs_included, "bdbsc": ex.bdbs_excluded,
                       "box-complement": ex.box_complement_excluded, "sat": ex.sat_included,
-                      "satc": ex.sat_excluded}[route]
+                      "satc": ex.sat_excluded, "corners": ex.corners_excluded}[route]
                 t = ex.Tensor(ops, x)
                 for _ in range(2):
                     fn(t, box)
