@@ -117,7 +117,7 @@ k_fused_pair(const T* __restrict__ in, T* __restrict__ out, int64_t outer, int64
       // streaming phase and would otherwise stall the row op on a global load
       constexpr int RPW = (U + NW - 1) / NW;  // rows per warp in the row op
       T tails[RPW];
-      if constexpr (MODE == ROW_EXCL) {
+      if constexpr (MODE != ROW_WIN) {
 #pragma unroll
         for (int i = 0; i < RPW; ++i) {
           const int rr = warp + i * NW;
@@ -213,18 +213,11 @@ k_fused_pair(const T* __restrict__ in, T* __restrict__ out, int64_t outer, int64
         // tests/parity.py); max has no inverse and keeps the scans below.
         // 8-byte rows with K2 >= 8 spill on this path (f64 512^3 box 16^3:
         // 0.58 vs 0.53 ms), so they keep the sub-chunk scans below.
-        constexpr bool ADD_EXCL = MODE == ROW_EXCL && std::is_same<Op, OpAdd>::value &&
-                                  (sizeof(T) == 4 || K2 <= 4);
-        if (MODE == ROW_WIN || (ADD_EXCL && kx == K2)) {
+        // (go_fused selects ROW_EXCL_ADD for + with kx == K2 and either 4-byte
+        // elements or K2 <= 4; it runs unrolled over the warp's rows like ROW_WIN)
+        constexpr bool ADD_EXCL = MODE == ROW_EXCL_ADD;
+        if constexpr (MODE == ROW_WIN || ADD_EXCL) {
           T rtot = T(0);
-          if constexpr (ADD_EXCL) {
-            T lt = a[0];
-#pragma unroll
-            for (int j = 1; j < C; ++j) lt = Op::apply(lt, a[j]);
-#pragma unroll
-            for (int d = 16; d >= 1; d >>= 1) lt = Op::apply(lt, __shfl_xor_sync(0xffffffffu, lt, d));
-            rtot = lt;
-          }
           // exact in-block scans along the row (blocks of K2 inside the chunk)
           constexpr int NBV = (K2 + VE - 1) / VE;
           VT nbv[NBV];  // neighbour's first block, raw
@@ -256,13 +249,20 @@ k_fused_pair(const T* __restrict__ in, T* __restrict__ out, int64_t outer, int64
               }
             }
           }
+          if constexpr (ADD_EXCL) {
+            // block heads hold the in-block suffix at the block start = the
+            // block total (the stitch never touches block starts): the row
+            // total is M2-1 adds and a warp reduction, off the scan chains
+            T lt = a[0];
+#pragma unroll
+            for (int j = 1; j < M2; ++j) lt = Op::apply(lt, a[j * K2]);
+#pragma unroll
+            for (int d = 16; d >= 1; d >>= 1) lt = Op::apply(lt, __shfl_xor_sync(0xffffffffu, lt, d));
+            rtot = lt;
+          }
           __syncwarp();
           T etail = T(0);
-          if constexpr (ADD_EXCL) {
-#pragma unroll
-            for (int i = 0; i < RPW; ++i)
-              if (ri == i) etail = tails[i];
-          }
+          if constexpr (ADD_EXCL) etail = tails[ri];
 #pragma unroll
           for (int v = 0; v < CV; ++v) {
             VT q;
@@ -473,6 +473,19 @@ int go_fused(const T* in, T* out, int64_t outer, int64_t n1, int64_t n2, int64_t
         return -1;
     }
   } else {
+    // + with a cubic box: row total minus the exact windowed row op (8-byte
+    // elements only for k <= 4: larger windows spill on that path)
+    if constexpr (std::is_same<Op, OpAdd>::value) {
+      if (k2 == k1 && (sizeof(T) == 4 || k1 <= 4)) {
+        switch (n2) {
+          case 256: return pick_k1<T, Op, 8, ROW_EXCL_ADD>(in, out, outer, n1, k1, k2, nullptr, Tail, s);
+          case 512: return pick_k1<T, Op, 16, ROW_EXCL_ADD>(in, out, outer, n1, k1, k2, nullptr, Tail, s);
+          case 1024:
+            if constexpr (sizeof(T) == 4) return pick_k1<T, Op, 32, ROW_EXCL_ADD>(in, out, outer, n1, k1, k2, nullptr, Tail, s);
+            return -1;
+        }
+      }
+    }
     switch (n2) {
       case 256: return pick_k1<T, Op, 8, ROW_EXCL>(in, out, outer, n1, k1, k2, nullptr, Tail, s);
       case 512: return pick_k1<T, Op, 16, ROW_EXCL>(in, out, outer, n1, k1, k2, nullptr, Tail, s);
