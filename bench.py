@@ -373,6 +373,37 @@ def main():
                "ms_per_step": statistics.median(times) * 1e3, "steps": e_steps,
                "path": "exsum_run_host (pinned host in/out; H2D + compute + D2H per step)"}
 
+    if not args.no_e2e and world > 1:
+        # each rank: its own planes host->device, the sharded step (halo and
+        # reductions over NCCL), its output planes device->host; max over ranks
+        n_own = runner.n_own
+        host_in = torch.empty((n_own,) + tuple(ext[1:]), dtype=x.dtype, pin_memory=True)
+        host_in.copy_(x[:n_own])
+        host_out = torch.empty_like(host_in, pin_memory=True)
+
+        def e2e_step():
+            x[:n_own].copy_(host_in, non_blocking=True)
+            y = runner(x)
+            if y is not None and n_own > 0:
+                host_out.copy_(y, non_blocking=True)
+            torch.cuda.synchronize(dev)
+
+        e2e_step()
+        e_steps = max(1, min(args.steps, 3))
+        times = []
+        for _ in range(e_steps):
+            dist.barrier()
+            t0 = time.perf_counter()
+            e2e_step()
+            times.append(time.perf_counter() - t0)
+        tt = torch.tensor([statistics.median(times)], device=dev, dtype=torch.float64)
+        dist.all_reduce(tt, op=dist.ReduceOp.MAX)
+        sec = float(tt.item())
+        e2e = {"value": N / sec, "unit": UNIT, "h2d_bytes_per_step": N * es,
+               "d2h_bytes_per_step": N * es, "ms_per_step": sec * 1e3, "steps": e_steps,
+               "path": "per rank: own planes H2D (pinned) + ShardedRunner + own output D2H; "
+                       "max over ranks; bytes summed over ranks"}
+
     cpu = None
     if not args.no_cpu and rank == 0 and world == 1:
         nthreads = os.cpu_count() or 1
