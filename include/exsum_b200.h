@@ -115,6 +115,39 @@ int exsum_box_complement_excluded(const void *in, void *out, int dtype, int op, 
 int exsum_windowed_pass(const void *in, void *out, int dtype, int op, int d,
                         const int64_t *ext, int axis, int64_t k, void *stream);
 
+/* ---- building blocks, device arrays, stream-ordered ----
+ * op: EXSUM_ADD / EXSUM_MAX / EXSUM_MODADD (with `modulus`). */
+
+/* MonoidOps.accumulate(arr, axis, reverse) (monoid.py:156-159, 196-198, 224-226,
+ * 280-283) out of place or in place (in == out): a sequential running fold
+ * along `axis` -- and with it prefix_along_dim / suffix_along_dim
+ * (scan.py:113-120) on a reduced slice. */
+int exsum_scan_workspace_bytes(int dtype, int op, int64_t modulus, int d, const int64_t *ext,
+                               int axis, size_t *bytes);
+int exsum_scan_axis(const void *in, void *out, int dtype, int op, int64_t modulus, int d,
+                    const int64_t *ext, int axis, int reverse, void *ws, size_t ws_bytes,
+                    void *stream);
+
+/* add_contribution(src, dst, dim, offset) (excluded.py:111-126): dst has extents
+ * ext; src is the reduced slice of shape ext[dim:]; dst[.., x_dim, ..] (+)=
+ * src[x_dim + offset, ..] wherever 0 <= x_dim + offset < ext[dim]. */
+int exsum_add_contribution(const void *src, void *dst, int dtype, int op, int64_t modulus, int d,
+                           const int64_t *ext, int dim, int64_t offset, void *stream);
+
+/* MonoidOps bulk kernels on n elements: kind 0 combine_into(dst, src) (also
+ * rcombine_into: every operator is commutative), 1 subtract_into(dst, src),
+ * 2 rsubtract_scalar(*scalar, dst) with `scalar` a host pointer to one element.
+ * Kinds 1 and 2 need an inverse (EXSUM_ECONFIG for max). */
+int exsum_elementwise(void *dst, const void *src, const void *scalar, int dtype, int op,
+                      int64_t modulus, int kind, int64_t n, void *stream);
+
+/* MonoidOps.fold (monoid.py:161-164, 200-204, 229-232, 284-286) of n elements into
+ * one element of device memory `result` (deterministic tree; float32 accumulates
+ * in float64; the identity when n == 0). */
+size_t exsum_fold_workspace_bytes(void);
+int exsum_fold(const void *in, void *result, int dtype, int op, int64_t modulus, int64_t n,
+               void *ws, size_t ws_bytes, void *stream);
+
 /* Host-buffer convenience: copies h_in to the device, runs `route`, copies
  * the result to h_out and synchronizes.  Device buffers are cached per
  * device between calls.  This is the call a host-side plug-in makes

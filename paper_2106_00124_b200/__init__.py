@@ -42,6 +42,13 @@ from .routes import (
     sat_included,
     windowed_sum_axis,
 )
+from .pieces import (
+    add_contribution,
+    bdbs_along_dim,
+    prefix_along_dim,
+    reduced_slice,
+    suffix_along_dim,
+)
 from .tensor import Tensor, crop_to, normalize_box, pad_to_box_multiple, validate_extents
 
 __version__ = "0.1.0"
@@ -54,6 +61,7 @@ __all__ = [
     "box_complement_excluded", "check_algorithm_config", "corners_excluded",
     "corners_spine_excluded", "crop_to", "normalize_box",
     "pad_to_box_multiple", "register_with_reference", "resolve_algorithm", "resolve_monoid",
-    "sat_excluded", "sat_included",
+    "sat_excluded", "sat_included", "add_contribution", "bdbs_along_dim", "prefix_along_dim",
+    "reduced_slice", "suffix_along_dim",
     "validate_extents", "windowed_sum_axis",
 ]

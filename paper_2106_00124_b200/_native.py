@@ -44,6 +44,12 @@ EXPORTS = (
     "exsum_profile_enable",
     "exsum_profile_count",
     "exsum_profile_get",
+    "exsum_scan_workspace_bytes",
+    "exsum_scan_axis",
+    "exsum_add_contribution",
+    "exsum_elementwise",
+    "exsum_fold_workspace_bytes",
+    "exsum_fold",
     "exsum_shard_workspace_bytes",
     "exsum_shard_axis0_pass",
     "exsum_bdbs_finish",
@@ -91,6 +97,17 @@ def load():
         L.exsum_route.restype = ci
         L.exsum_route_host.argtypes = [ci, vp, vp, ci, ci, i64, ci, i64p, i64p]
         L.exsum_route_host.restype = ci
+        L.exsum_scan_workspace_bytes.argtypes = [ci, ci, i64, ci, i64p, ci, ctypes.POINTER(sz)]
+        L.exsum_scan_workspace_bytes.restype = ci
+        L.exsum_scan_axis.argtypes = [vp, vp, ci, ci, i64, ci, i64p, ci, ci, vp, sz, vp]
+        L.exsum_scan_axis.restype = ci
+        L.exsum_add_contribution.argtypes = [vp, vp, ci, ci, i64, ci, i64p, ci, i64, vp]
+        L.exsum_add_contribution.restype = ci
+        L.exsum_elementwise.argtypes = [vp, vp, vp, ci, ci, i64, ci, i64, vp]
+        L.exsum_elementwise.restype = ci
+        L.exsum_fold_workspace_bytes.restype = sz
+        L.exsum_fold.argtypes = [vp, vp, ci, ci, i64, i64, vp, sz, vp]
+        L.exsum_fold.restype = ci
         L.exsum_release_cache.restype = ci
         L.exsum_profile_enable.argtypes = [ci]
         L.exsum_profile_enable.restype = ci

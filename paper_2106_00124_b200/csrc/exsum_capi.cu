@@ -947,6 +947,119 @@ int exsum_run_host(int route, const void* h_in, void* h_out, int dtype, int op, 
   return exsum_route_host(route, h_in, h_out, dtype, op, 0, d, ext, box);
 }
 
+// ------------------------------------------------------- building blocks --
+
+int exsum_scan_workspace_bytes(int dtype, int op, int64_t modulus, int d, const int64_t* ext,
+                               int axis, size_t* bytes) {
+  g_err.clear();
+  int rc = check_types(dtype, op, op == EXSUM_MODADD ? modulus : 0);
+  if (rc) return rc;
+  if (d < 1 || d > EXSUM_MAX_DIMS || !ext) return fail(EXSUM_EUSAGE, "bad extents");
+  if (axis < 0 || axis >= d) return fail(EXSUM_EUSAGE, "axis out of range");
+  for (int i = 0; i < d; ++i)
+    if (ext[i] < 1) return fail(EXSUM_EUSAGE, "every extent must be >= 1");
+  Arena sizing(nullptr);
+  int launches = 0;
+  rc = scan_view(dtype, (const void*)1, (void*)2, prod(ext, 0, axis), ext[axis],
+                 prod(ext, axis + 1, d), sizing, nullptr, &launches,
+                 op == EXSUM_MAX ? EXSUM_MAX : EXSUM_ADD, 0);
+  if (rc) return rc;
+  if (bytes) *bytes = sizing.off;
+  return EXSUM_OK;
+}
+
+int exsum_scan_axis(const void* in, void* out, int dtype, int op, int64_t modulus, int d,
+                    const int64_t* ext, int axis, int reverse, void* ws, size_t ws_bytes,
+                    void* stream) {
+  size_t need = 0;
+  int rc = exsum_scan_workspace_bytes(dtype, op, modulus, d, ext, axis, &need);
+  if (rc) return rc;
+  if (!in || !out) return fail(EXSUM_EUSAGE, "null array pointer");
+  if (need > 0 && (ws == nullptr || ws_bytes < need))
+    return fail(EXSUM_EUSAGE, "workspace too small (see exsum_scan_workspace_bytes)");
+  cudaStream_t st = (cudaStream_t)stream;
+  Arena ar(ws);
+  int launches = 0;
+  // ModAddOps.accumulate (monoid.py:280-283): raw int64 running sum, then
+  // np.remainder over the whole array
+  rc = scan_view(dtype, in, out, prod(ext, 0, axis), ext[axis], prod(ext, axis + 1, d), ar, st,
+                 &launches, op == EXSUM_MAX ? EXSUM_MAX : EXSUM_ADD, reverse != 0);
+  if (rc) return rc;
+  if (op == EXSUM_MODADD) launches += launch_mod_map(out, out, prod(ext, 0, d), 0, make_fastmod(modulus), nullptr, st);
+  g_last_launches = launches;
+  g_total_launches += launches;
+  return cuda_check("scan");
+}
+
+int exsum_add_contribution(const void* src, void* dst, int dtype, int op, int64_t modulus, int d,
+                           const int64_t* ext, int dim, int64_t offset, void* stream) {
+  g_err.clear();
+  int rc = check_types(dtype, op, op == EXSUM_MODADD ? modulus : 0);
+  if (rc) return rc;
+  if (d < 1 || d > EXSUM_MAX_DIMS || !ext) return fail(EXSUM_EUSAGE, "bad extents");
+  if (dim < 0 || dim >= d) return fail(EXSUM_EUSAGE, "dimension out of range");
+  if (!src || !dst) return fail(EXSUM_EUSAGE, "null array pointer");
+  for (int i = 0; i < d; ++i)
+    if (ext[i] < 1) return fail(EXSUM_EUSAGE, "every extent must be >= 1");
+  const int launches = launch_add_contribution(dtype, op, make_fastmod(modulus), src, dst,
+                                               prod(ext, 0, dim), ext[dim], prod(ext, dim + 1, d),
+                                               offset, (cudaStream_t)stream);
+  if (launches < 0) return fail(EXSUM_ECONFIG, "no kernel for this dtype/operator");
+  g_last_launches = launches;
+  g_total_launches += launches;
+  return cuda_check("add_contribution");
+}
+
+int exsum_elementwise(void* dst, const void* src, const void* scalar, int dtype, int op,
+                      int64_t modulus, int kind, int64_t n, void* stream) {
+  g_err.clear();
+  int rc = check_types(dtype, op, op == EXSUM_MODADD ? modulus : 0);
+  if (rc) return rc;
+  if (kind < 0 || kind > 2) return fail(EXSUM_EUSAGE, "unknown element operation");
+  if (kind > 0 && op == EXSUM_MAX)
+    return fail(EXSUM_ECONFIG, "monoid 'max-i64' has no inverse");  // monoid.py:72-78
+  if (n < 0 || !dst || (kind < 2 && !src) || (kind == 2 && !scalar))
+    return fail(EXSUM_EUSAGE, "bad element-operation arguments");
+  if (n == 0) return EXSUM_OK;
+  const int launches = launch_elementwise(dtype, op, make_fastmod(modulus), dst, src, scalar, kind,
+                                          n, (cudaStream_t)stream);
+  if (launches < 0) return fail(EXSUM_ECONFIG, "no kernel for this dtype/operator");
+  g_last_launches = launches;
+  g_total_launches += launches;
+  return cuda_check("elementwise");
+}
+
+size_t exsum_fold_workspace_bytes(void) { return (size_t)reduce_partials_count() * 8 + 512; }
+
+int exsum_fold(const void* in, void* result, int dtype, int op, int64_t modulus, int64_t n,
+               void* ws, size_t ws_bytes, void* stream) {
+  g_err.clear();
+  int rc = check_types(dtype, op, op == EXSUM_MODADD ? modulus : 0);
+  if (rc) return rc;
+  if (n < 0 || !result || (n > 0 && !in)) return fail(EXSUM_EUSAGE, "bad fold arguments");
+  if (!ws || ws_bytes < exsum_fold_workspace_bytes())
+    return fail(EXSUM_EUSAGE, "workspace too small (see exsum_fold_workspace_bytes)");
+  cudaStream_t st = (cudaStream_t)stream;
+  const size_t es = dtype_size(dtype);
+  if (n == 0) {  // MonoidOps.fold of an empty array: the identity
+    static const float f0 = 0.0f;
+    static const double d0 = 0.0;
+    static const int64_t i0 = 0, imin = (int64_t)0x8000000000000000ULL;
+    const void* idv = dtype == EXSUM_F32 ? (const void*)&f0 : dtype == EXSUM_F64 ? (const void*)&d0
+                      : op == EXSUM_MAX ? (const void*)&imin : (const void*)&i0;
+    cudaMemcpyAsync(result, idv, es, cudaMemcpyHostToDevice, st);
+    return cuda_check("fold");
+  }
+  char* w = (char*)ws;
+  void* acc = w;  // 8 bytes, then the partials
+  void* partials = w + 256;
+  int launches = launch_total(dtype, op == EXSUM_MAX ? EXSUM_MAX : EXSUM_ADD, in, n, partials, acc, st);
+  launches += launch_fold_result(dtype, op, make_fastmod(modulus), acc, result, st);
+  g_last_launches = launches;
+  g_total_launches += launches;
+  return cuda_check("fold");
+}
+
 int exsum_profile_enable(int on) {
   g_prof.on = on != 0;
   g_prof.recs.clear();

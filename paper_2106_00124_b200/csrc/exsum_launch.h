@@ -147,6 +147,17 @@ struct SliceSpec {
 int launch_copy_slice(const void* in, void* out, const SliceSpec& sp, int64_t count,
                       cudaStream_t s);
 
+// ------------------------------------------------ building blocks (pieces.cu)
+// op: 0 add, 1 max (int64), 2 mod-add (int64, fm)
+int launch_add_contribution(int dtype, int op, const FastMod& fm, const void* src, void* dst,
+                            int64_t outer, int64_t n, int64_t inner, int64_t offset,
+                            cudaStream_t s);
+// kind 0 combine_into, 1 subtract_into, 2 rsubtract_scalar (scalar read from host)
+int launch_elementwise(int dtype, int op, const FastMod& fm, void* dst, const void* src,
+                       const void* scalar_host, int kind, int64_t n, cudaStream_t s);
+int launch_fold_result(int dtype, int op, const FastMod& fm, const void* acc, void* out,
+                       cudaStream_t s);
+
 size_t dtype_size(int dtype);
 int num_sms();
 

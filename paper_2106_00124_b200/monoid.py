@@ -45,6 +45,37 @@ class MonoidOps:
     def subtract(self, a, b):
         raise ConfigurationError(f"monoid {self.name!r} has no inverse")
 
+    # -- bulk kernels (monoid.py:66-104): in place, on the GPU (pieces.py) -------
+    def combine_into(self, dst, src):
+        from . import pieces
+
+        pieces.combine_into(self, dst, src)
+
+    def rcombine_into(self, dst, src):
+        from . import pieces
+
+        pieces.rcombine_into(self, dst, src)
+
+    def subtract_into(self, dst, src):
+        from . import pieces
+
+        pieces.subtract_into(self, dst, src)
+
+    def rsubtract_scalar(self, total, dst):
+        from . import pieces
+
+        pieces.rsubtract_scalar(self, total, dst)
+
+    def accumulate(self, arr, axis, reverse=False):
+        from . import pieces
+
+        pieces.accumulate(self, arr, axis, reverse)
+
+    def fold(self, arr):
+        from . import pieces
+
+        return pieces.fold(self, arr)
+
     def __repr__(self):
         return f"{type(self).__name__}({self.name})"
 
