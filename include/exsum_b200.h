@@ -155,7 +155,17 @@ int exsum_fold(const void *in, void *result, int dtype, int op, int64_t modulus,
 int exsum_run_host(int route, const void *h_in, void *h_out, int dtype, int op, int d,
                    const int64_t *ext, const int64_t *box);
 
-/* Release the device buffers cached by exsum_run_host. */
+/* A stream of `count` independent arrays of the same extents through one route
+ * (AlgorithmInfo.run over many inputs): h_in[i] -> h_out[i].  Two device slots
+ * and separate copy streams pipeline the host->device copy of array i+1, the
+ * compute of array i and the device->host copy of array i-1 (the copy engines
+ * run both directions at once).  Returns after the last copy lands.  Pinned
+ * host buffers give full PCIe bandwidth. */
+int exsum_route_host_batch(int route, int count, const void *const *h_in, void *const *h_out,
+                           int dtype, int op, int64_t modulus, int d, const int64_t *ext,
+                           const int64_t *box);
+
+/* Release the device buffers cached by exsum_run_host / exsum_route_host_batch. */
 int exsum_release_cache(void);
 
 /* Number of kernels the last successful call on this thread launched

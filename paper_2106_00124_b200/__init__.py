@@ -38,6 +38,7 @@ from .routes import (
     corners_spine_excluded,
     register_with_reference,
     resolve_algorithm,
+    run_many,
     sat_excluded,
     sat_included,
     windowed_sum_axis,
@@ -62,6 +63,6 @@ __all__ = [
     "corners_spine_excluded", "crop_to", "normalize_box",
     "pad_to_box_multiple", "register_with_reference", "resolve_algorithm", "resolve_monoid",
     "sat_excluded", "sat_included", "add_contribution", "bdbs_along_dim", "prefix_along_dim",
-    "reduced_slice", "suffix_along_dim",
+    "reduced_slice", "run_many", "suffix_along_dim",
     "validate_extents", "windowed_sum_axis",
 ]

@@ -33,6 +33,7 @@ EXPORTS = (
     "exsum_route_workspace_bytes",
     "exsum_route",
     "exsum_route_host",
+    "exsum_route_host_batch",
     "exsum_bdbs_included",
     "exsum_bdbsc_excluded",
     "exsum_box_complement_excluded",
@@ -97,6 +98,9 @@ def load():
         L.exsum_route.restype = ci
         L.exsum_route_host.argtypes = [ci, vp, vp, ci, ci, i64, ci, i64p, i64p]
         L.exsum_route_host.restype = ci
+        L.exsum_route_host_batch.argtypes = [ci, ci, ctypes.POINTER(vp), ctypes.POINTER(vp), ci,
+                                             ci, i64, ci, i64p, i64p]
+        L.exsum_route_host_batch.restype = ci
         L.exsum_scan_workspace_bytes.argtypes = [ci, ci, i64, ci, i64p, ci, ctypes.POINTER(sz)]
         L.exsum_scan_workspace_bytes.restype = ci
         L.exsum_scan_axis.argtypes = [vp, vp, ci, ci, i64, ci, i64p, ci, ci, vp, sz, vp]

@@ -818,6 +818,24 @@ struct HostCache {
   std::vector<cudaStream_t> stream;
 };
 
+// exsum_route_host_batch: two device slots and three streams per device, so
+// the copy engines run both directions at once (PCIe is full duplex: ~56 GB/s
+// each way, ~100 GB/s together, measured on B200 boxes) while a slot computes.
+struct BatchSlot {
+  DevBuf in, out, ws;
+  cudaEvent_t h2d = nullptr, done = nullptr, d2h = nullptr;
+};
+struct BatchCache {
+  std::mutex mu;
+  std::vector<int> dev;
+  std::vector<BatchSlot> slots;  // 2 per device
+  std::vector<cudaStream_t> streams;  // 3 per device: h2d, compute, d2h
+};
+BatchCache& batch_cache() {
+  static BatchCache c;
+  return c;
+}
+
 HostCache& host_cache() {
   static HostCache c;
   return c;
@@ -940,6 +958,70 @@ int exsum_route_host(int route, const void* h_in, void* h_out, int dtype, int op
   cudaMemcpyAsync(h_out, c.out[slot].p, bytes, cudaMemcpyDeviceToHost, st);
   if (cudaStreamSynchronize(st) != cudaSuccess) return cuda_check("cudaStreamSynchronize");
   return cuda_check("host path");
+}
+
+int exsum_route_host_batch(int route, int count, const void* const* h_in, void* const* h_out,
+                           int dtype, int op, int64_t modulus, int d, const int64_t* ext,
+                           const int64_t* box) {
+  g_err.clear();
+  Shape s;
+  int rc = validate(route, dtype, op, modulus, d, ext, box, &s);
+  if (rc) return rc;
+  if (count < 0 || (count > 0 && (!h_in || !h_out))) return fail(EXSUM_EUSAGE, "bad batch arrays");
+  for (int i = 0; i < count; ++i)
+    if (!h_in[i] || !h_out[i]) return fail(EXSUM_EUSAGE, "null host pointer in batch");
+  if (count == 0) return EXSUM_OK;
+  size_t ws_bytes = 0;
+  rc = exsum_route_workspace_bytes(route, dtype, op, modulus, d, ext, box, &ws_bytes);
+  if (rc) return rc;
+  int dev = 0;
+  if (cudaGetDevice(&dev) != cudaSuccess) return cuda_check("cudaGetDevice");
+  BatchCache& c = batch_cache();
+  std::lock_guard<std::mutex> lock(c.mu);
+  size_t di = 0;
+  while (di < c.dev.size() && c.dev[di] != dev) ++di;
+  if (di == c.dev.size()) {
+    c.dev.push_back(dev);
+    for (int k = 0; k < 2; ++k) {
+      BatchSlot b;
+      if (cudaEventCreateWithFlags(&b.h2d, cudaEventDisableTiming) != cudaSuccess ||
+          cudaEventCreateWithFlags(&b.done, cudaEventDisableTiming) != cudaSuccess ||
+          cudaEventCreateWithFlags(&b.d2h, cudaEventDisableTiming) != cudaSuccess)
+        return cuda_check("cudaEventCreate");
+      c.slots.push_back(b);
+    }
+    for (int k = 0; k < 3; ++k) {
+      cudaStream_t st;
+      if (cudaStreamCreateWithFlags(&st, cudaStreamNonBlocking) != cudaSuccess)
+        return cuda_check("cudaStreamCreate");
+      c.streams.push_back(st);
+    }
+  }
+  BatchSlot* slot = &c.slots[2 * di];
+  cudaStream_t s_in = c.streams[3 * di], s_run = c.streams[3 * di + 1], s_out = c.streams[3 * di + 2];
+  const size_t bytes = (size_t)s.N * dtype_size(dtype);
+  const int nslots = count > 1 ? 2 : 1;
+  for (int k = 0; k < nslots; ++k)
+    if (slot[k].in.reserve(bytes) || slot[k].out.reserve(bytes) ||
+        slot[k].ws.reserve(ws_bytes > 0 ? ws_bytes : 256))
+      return fail(EXSUM_ECUDA, "cudaMalloc failed for batch buffers");
+  for (int i = 0; i < count; ++i) {
+    BatchSlot& b = slot[i % nslots];
+    if (i >= nslots) cudaStreamWaitEvent(s_in, b.done, 0);  // compute of i-2 released `in`
+    cudaMemcpyAsync(b.in.p, h_in[i], bytes, cudaMemcpyHostToDevice, s_in);
+    cudaEventRecord(b.h2d, s_in);
+    cudaStreamWaitEvent(s_run, b.h2d, 0);
+    if (i >= nslots) cudaStreamWaitEvent(s_run, b.d2h, 0);  // D2H of i-2 released `out`
+    rc = run_device(route, b.in.p, b.out.p, dtype, op, modulus, d, ext, box, b.ws.p, b.ws.cap,
+                    s_run);
+    if (rc) return rc;
+    cudaEventRecord(b.done, s_run);
+    cudaStreamWaitEvent(s_out, b.done, 0);
+    cudaMemcpyAsync(h_out[i], b.out.p, bytes, cudaMemcpyDeviceToHost, s_out);
+    cudaEventRecord(b.d2h, s_out);
+  }
+  if (cudaStreamSynchronize(s_out) != cudaSuccess) return cuda_check("cudaStreamSynchronize");
+  return cuda_check("host batch");
 }
 
 int exsum_run_host(int route, const void* h_in, void* h_out, int dtype, int op, int d,
@@ -1123,6 +1205,19 @@ int exsum_box_complement_finish(const void* in, void* out, int dtype, int op, in
 }
 
 int exsum_release_cache(void) {
+  {
+    BatchCache& b = batch_cache();
+    std::lock_guard<std::mutex> lock(b.mu);
+    int cur = 0;
+    cudaGetDevice(&cur);
+    for (size_t i = 0; i < b.slots.size(); ++i) {
+      cudaSetDevice(b.dev[i / 2]);
+      b.slots[i].in.release();
+      b.slots[i].out.release();
+      b.slots[i].ws.release();
+    }
+    cudaSetDevice(cur);
+  }
   HostCache& c = host_cache();
   std::lock_guard<std::mutex> lock(c.mu);
   int cur = 0;

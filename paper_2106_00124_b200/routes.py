@@ -109,6 +109,52 @@ def run_host(route: str, a: np.ndarray, dtype: str, op: str, ext, k, out=None,
     return out
 
 
+def run_host_batch(route: str, arrays, dtype: str, op: str, ext, k, outs=None,
+                   modulus: int = 0):
+    """Run ``route`` over a list of same-shaped host arrays with the copies of
+    consecutive arrays overlapped (exsum_route_host_batch); returns the outputs."""
+    import ctypes
+
+    arrays = [np.ascontiguousarray(a) for a in arrays]
+    if outs is None:
+        outs = [np.empty_like(a) for a in arrays]
+    for a, o in zip(arrays, outs):
+        if a.shape != tuple(ext) or o.shape != a.shape or o.dtype != a.dtype or \
+                not o.flags.c_contiguous:
+            raise UsageError("every input and output must have the batch's extents and dtype")
+    L = _native.load()
+    n = len(arrays)
+    pin = (ctypes.c_void_p * n)(*[a.ctypes.data for a in arrays])
+    pout = (ctypes.c_void_p * n)(*[o.ctypes.data for o in outs])
+    _native.check(L.exsum_route_host_batch(_native.ROUTE[route], n, pin, pout,
+                                           _native.DTYPE[dtype], _native.OP[op], int(modulus),
+                                           len(ext), _native.i64_array(ext), _native.i64_array(k)))
+    return outs
+
+
+def run_many(algo: str, tensors, box):
+    """One registry entry over many same-shaped tensors (AlgorithmInfo.run per
+    tensor), returning the result tensors in order.  Host (numpy) tensors go
+    through exsum_route_host_batch, which overlaps the host->device copy of the
+    next array with the device->host copy of the previous one; device tensors
+    run back to back on the current stream."""
+    tensors = list(tensors)
+    if not tensors:
+        return []
+    if algo in ("corners", "corners-spine"):
+        return [ALGORITHMS[algo].run(t, box) for t in tensors]
+    resolve_algorithm(algo)
+    prepared = [_prepare(t, box, algo) for t in tensors]
+    if len({(p[0], p[1], p[2], p[3], p[4]) for p in prepared}) != 1:
+        raise UsageError("run_many needs tensors of one shape, dtype and monoid")
+    dtype, op, ext, k, m = prepared[0]
+    if any(is_torch(t.data) for t in tensors):
+        return [ALGORITHMS[algo].run(t, box) for t in tensors]
+    outs = run_host_batch(algo, [np.asarray(t.data) for t in tensors], dtype, op, ext, k,
+                          modulus=m)
+    return [_rewrap(t, o) for t, o in zip(tensors, outs)]
+
+
 def _route(route, t, box):
     dtype, op, ext, k, m = _prepare(t, box, route)
     data = t.data

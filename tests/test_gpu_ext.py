@@ -212,3 +212,28 @@ def test_corners_vs_oracle_and_box_complement(ex, mono):
             assert np.array_equal(got, want), (mono, shape)
             # and the strong excluded sum is the same whichever decomposition
             assert np.array_equal(got, _run(ex, "box-complement", mono, a, box))
+
+
+def test_run_many_host_batch_matches_single_calls(ex):
+    """exsum_route_host_batch: pipelined copies, same results as one call each."""
+    rng = np.random.default_rng(21)
+    for algo, mono, shape, box in [("box-complement", "add-f32", (40, 33, 256), (4, 3, 16)),
+                                   ("bdbsc", "add-i64", (17, 64, 9), (3, 8, 2)),
+                                   ("sat", "mod-add:97", (30, 40), (5, 7)),
+                                   ("bdbs", "max-i64", (1000,), (33,)),
+                                   ("corners", "add-f64", (20, 30), (4, 5))]:
+        ops = _mono(ex, mono)
+        arrs = []
+        for _ in range(5):
+            if mono.startswith("add-f"):
+                a = rng.random(shape).astype(ops.dtype)
+            else:
+                a = rng.integers(-1000, 1000, size=shape, dtype=np.int64)
+            arrs.append(ex.Tensor(ops, a))
+        outs = ex.run_many(algo, arrs, box)
+        for t, o in zip(arrs, outs):
+            want = _fn(ex, algo)(t, box).data
+            assert _bits_equal(np.asarray(o.data), np.asarray(want)), algo
+    with pytest.raises(ex.UsageError):
+        ex.run_many("bdbs", [ex.Tensor(ex.IntAddOps(), np.zeros((3, 4), dtype=np.int64)),
+                             ex.Tensor(ex.IntAddOps(), np.zeros((4, 3), dtype=np.int64))], (2, 2))
