@@ -41,6 +41,16 @@ namespace exsum {
 // K1: window along axis d-2 (compile time); the ROW_WIN row op uses the same
 // window along the row (K2 == K1, the cubic boxes of the BASELINE configs);
 // ROW_EXCL takes any shift kx at run time.
+#ifndef FP_NARROW_C
+#define FP_NARROW_C 8
+#endif
+// Rows per streaming unit: 16 (a multiple of K1) for wide rows; narrow rows
+// (C <= 8: 64-thread CTAs whose shared ring and stage bound the CTAs per SM)
+// take 8-row units where K1 allows, doubling the resident CTAs.
+__host__ __device__ constexpr int fp_unit_rows(int C, int K1) {
+  return (C <= FP_NARROW_C && K1 <= 8) ? 8 : (16 / K1 > 0 ? 16 / K1 : 1) * K1;
+}
+
 template <class T, class Op, int C, int K1, int MODE, int TV>
 __global__ void __launch_bounds__(32 * C / TV, 1)
 k_fused_pair(const T* __restrict__ in, T* __restrict__ out, int64_t outer, int64_t n1,
@@ -56,7 +66,7 @@ k_fused_pair(const T* __restrict__ in, T* __restrict__ out, int64_t outer, int64
   constexpr int ROWP = 32 * CH;        // padded row length (elements)
   constexpr int K2 = K1;
   constexpr int M2 = C / K2;           // row-op blocks per lane chunk
-  constexpr int G = 16 / K1 > 0 ? 16 / K1 : 1;  // blocks per unit
+  constexpr int G = fp_unit_rows(C, K1) / K1;  // blocks per unit
   constexpr int U = G * K1;            // rows per unit: register tile, stage, prefetch granule
   static_assert(C % VE == 0 && C % K2 == 0, "shape");
   typedef Vec<T, VE> VT;  // row-op vectors
@@ -420,7 +430,7 @@ int go_pair(const T* in, T* out, int64_t outer, int64_t n1, int64_t kx,
   constexpr int CV = C / VE;
   constexpr int PSV = (CV + 1) | 1;
   constexpr int ROWP = 32 * PSV * VE;
-  constexpr int U = (16 / K1) * K1;
+  constexpr int U = fp_unit_rows(C, K1);
   const size_t smem = ((size_t)2 * U * N2 + (size_t)U * ROWP) * sizeof(T);
   if (smem > 220 * 1024) return -1;
   int per_sm = (int)((228 * 1024) / (smem + 1024));
