@@ -75,17 +75,26 @@ k_scan_rows(const T* in, T* out, int64_t rows, int64_t n, int64_t L, int64_t nse
     }
     __syncwarp();
     T acc = T(0);
-    for (int64_t xo = 0; xo < maxlen; xo += W) {
-      // 32 independent loads in flight, then the transpose into the tile
-      T v[32];
+    // 32 independent loads per chunk; the next chunk's loads are issued as soon
+    // as the current one is staged, so they overlap its scan and stores
+    T v[32];
 #pragma unroll
-      for (int r = 0; r < 32; ++r) {
-        const int64_t l = slen[wid][r];
-        v[r] = xo + lane < l ? ld1(in + sbase[wid][r] + dir * (xo + lane)) : T(0);
-      }
+    for (int r = 0; r < 32; ++r) {
+      const int64_t l = slen[wid][r];
+      v[r] = lane < l ? ld1(in + sbase[wid][r] + dir * lane) : T(0);
+    }
+    for (int64_t xo = 0; xo < maxlen; xo += W) {
 #pragma unroll
       for (int r = 0; r < 32; ++r) sm[r * STRIDE + lane] = v[r];
       __syncwarp();
+      if (xo + W < maxlen) {
+        const int64_t xn = xo + W + lane;
+#pragma unroll
+        for (int r = 0; r < 32; ++r) {
+          const int64_t l = slen[wid][r];
+          v[r] = xn < l ? ld1(in + sbase[wid][r] + dir * xn) : T(0);
+        }
+      }
       if (mylen > xo) {
         const int w = mylen - xo < W ? (int)(mylen - xo) : W;
         if (w == W) {
