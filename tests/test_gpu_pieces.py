@@ -115,6 +115,7 @@ def test_elementwise_and_fold(ex, name):
         exact = math.fsum(a.astype(np.float64).reshape(-1))
         assert abs(f - exact) <= 64 * np.finfo(a.dtype).eps * np.abs(a).sum()
     assert ops.fold(a[:0]) == ops.identity  # empty: the identity
+    assert ex.Tensor(ops, a).total_reduce() == f
 
 
 def test_reduced_slice_helpers(ex):
