@@ -17,7 +17,9 @@
  *   - work is stream-ordered on `stream` (a cudaStream_t; NULL = legacy
  *     default stream); the call returns after enqueueing;
  *   - no hidden device allocations on the device-pointer entry points: the
- *     caller passes a workspace of exsum_workspace_bytes() bytes;
+ *     caller passes a workspace of exsum_workspace_bytes() bytes (enough for
+ *     16-byte aligned arrays, as every CUDA allocation is, and for arrays off
+ *     that alignment, which run unfused kernels);
  *   - no CPU fallback: an unsupported dtype/operator is EXSUM_ECONFIG.
  *
  * Return codes map onto the reference's exceptions (errors.py:8-22):

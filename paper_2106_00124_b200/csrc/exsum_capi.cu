@@ -148,6 +148,10 @@ struct Arena {
   }
 };
 
+// The fused pass pair moves 16-byte vectors; a caller's array off that
+// alignment (a view into a larger buffer) takes the unfused kernels instead.
+bool aligned16(const void* p) { return ((uintptr_t)p & 15) == 0; }
+
 int64_t prod(const int64_t* e, int lo, int hi) {
   int64_t p = 1;
   for (int i = lo; i < hi; ++i) p *= e[i];
@@ -243,7 +247,8 @@ int route_bdbs(const Shape& s, int dtype, int op, const void* in, void* out, Are
   }
   const int d = s.d;
   const bool fused = p.count >= 2 && p.axes[p.count - 2] == d - 2 && p.axes[p.count - 1] == d - 1 &&
-                     fused_pair_ok(dtype, op, s.ext[d - 1], s.k[d - 2], s.k[d - 1], ROW_WIN);
+                     fused_pair_ok(dtype, op, s.ext[d - 1], s.k[d - 2], s.k[d - 1], ROW_WIN) &&
+                     aligned16(out) && (p.count > 2 || aligned16(in));
   PassPlan head = p;
   if (fused) head.count -= 2;
   // BDBSC total: folded into the first pass when a later pass applies it
@@ -347,7 +352,8 @@ int route_box_complement(const Shape& s, int dtype, int op, const void* src, voi
   void* T = ar.take((size_t)rows * es);
   PassPlan p = plan_passes(s, d - 1);  // W = windowed passes along axes 0..d-2
   const bool fused = p.count > 0 && p.axes[p.count - 1] == d - 2 &&
-                     fused_pair_ok(dtype, op, n, s.k[d - 2], s.k[d - 1], ROW_EXCL);
+                     fused_pair_ok(dtype, op, n, s.k[d - 2], s.k[d - 1], ROW_EXCL) &&
+                     aligned16(dst) && (p.count > 1 || aligned16(src));
   PassPlan head = p;
   if (fused) head.count -= 1;
   // R = reduction over the last axis, folded into the first W pass when
@@ -737,7 +743,8 @@ int stage_bc_finish(const Shape& s, int dtype, int op, const void* in, void* out
   for (int i = 0; i < p.count; ++i)
     if (p.axes[i] != 0) head.axes[head.count++] = p.axes[i];
   const bool fused = head.count > 0 && head.axes[head.count - 1] == d - 2 &&
-                     fused_pair_ok(dtype, op, s.ext[d - 1], s.k[d - 2], s.k[d - 1], ROW_EXCL);
+                     fused_pair_ok(dtype, op, s.ext[d - 1], s.k[d - 2], s.k[d - 1], ROW_EXCL) &&
+                     aligned16(out) && (head.count > 1 || aligned16(in));
   if (fused) head.count -= 1;
   return bc_finish(s, dtype, op, in, out, T, head, fused, nullptr, no_hook, ar, st, launches);
 }
@@ -861,9 +868,17 @@ int exsum_route_workspace_bytes(int route, int dtype, int op, int64_t modulus, i
   if (rc) return rc;
   Arena sizing(nullptr);
   int launches = 0;
-  rc = dispatch(route, s, dtype, op, modulus, (const void*)1, (void*)2, sizing, nullptr, &launches);
+  // the larger of the plans for 16-byte aligned arrays (every CUDA allocation)
+  // and for arrays off that alignment (unfused kernels; the two differ only
+  // for 2-D box-complement); run_device re-plans with the caller's pointers
+  rc = dispatch(route, s, dtype, op, modulus, (const void*)256, (void*)512, sizing, nullptr,
+                &launches);
   if (rc) return rc;
-  if (bytes) *bytes = sizing.off;
+  Arena sizing_u(nullptr);
+  rc = dispatch(route, s, dtype, op, modulus, (const void*)8, (void*)24, sizing_u, nullptr,
+                &launches);
+  if (rc) return rc;
+  if (bytes) *bytes = sizing.off > sizing_u.off ? sizing.off : sizing_u.off;
   return EXSUM_OK;
 }
 
@@ -1172,7 +1187,7 @@ int exsum_shard_workspace_bytes(int stage, int dtype, int op, int d, const int64
   g_err.clear();
   Arena sizing(nullptr);
   int launches = 0;
-  int rc = run_stage(stage, dtype, op, d, ext, box, n_out, extra_kind, (const void*)1, (void*)2,
+  int rc = run_stage(stage, dtype, op, d, ext, box, n_out, extra_kind, (const void*)256, (void*)512,
                      (const void*)3, (void*)4, sizing, nullptr, &launches);
   if (rc) return rc;
   if (bytes) *bytes = sizing.off;

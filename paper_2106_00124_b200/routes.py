@@ -77,8 +77,12 @@ def run_device(route: str, x, dtype: str, op: str, ext, k, out=None, modulus: in
     if not x.is_cuda:
         raise UsageError("run_device needs a CUDA tensor")
     x = x.contiguous()
+    if x.data_ptr() % 16:
+        x = x.clone()  # a view off 16-byte alignment: the fused kernels need aligned rows
     if out is None:
         out = torch.empty_like(x)
+    elif out.data_ptr() % 16 or not out.is_contiguous():
+        raise UsageError("out must be a contiguous, 16-byte aligned CUDA tensor")
     L = _native.load()
     ws_bytes = _native.workspace_bytes(route, dtype, op, ext, k, modulus)
     with torch.cuda.device(x.device):
