@@ -117,3 +117,100 @@ def test_no_writes_outside_the_call_regions(ex, shift):
             assert np.array_equal(got, want), (shape, box, mono, route)
         count += 1
     assert count > 300
+
+
+def test_building_block_guards(ex):
+    """exsum_scan_axis / exsum_add_contribution / exsum_elementwise / exsum_fold
+    on guarded, aligned and misaligned regions."""
+    import torch
+
+    from paper_2106_00124_b200 import _native
+
+    L = _native.load()
+    rng = np.random.default_rng(32)
+    st = torch.cuda.current_stream().cuda_stream
+    for shape in [(7,), (5, 9), (3, 300, 2), (2, 5000), (4, 6, 10)]:
+        n = int(np.prod(shape))
+        for dcode, dt, op, m in [(0, np.float32, 0, 0), (1, np.float64, 0, 0), (2, np.int64, 0, 0),
+                                 (2, np.int64, 1, 0), (2, np.int64, 2, 97)]:
+            for shift in (0, 1):
+                a = (rng.standard_normal(shape).astype(dt) if np.dtype(dt).kind == "f"
+                     else rng.integers(-1000, 1000, size=shape, dtype=np.int64))
+                es = np.dtype(dt).itemsize
+                base = np.zeros(n + 2 * GUARD, dtype=dt)
+                base[GUARD + shift:GUARD + shift + n] = a.reshape(-1)
+                buf = torch.from_numpy(base).cuda()
+                ptr = buf.data_ptr() + (GUARD + shift) * es
+                ext = _native.i64_array(shape)
+                for axis in range(len(shape)):
+                    need = ctypes.c_size_t(0)
+                    _native.check(L.exsum_scan_workspace_bytes(dcode, op, m, len(shape), ext, axis,
+                                                               ctypes.byref(need)))
+                    ws = torch.full((int(need.value) + 2 * 4096,), 0x5A, dtype=torch.uint8,
+                                    device="cuda")
+                    _native.check(L.exsum_scan_axis(ptr, ptr, dcode, op, m, len(shape), ext, axis,
+                                                    axis % 2, ws.data_ptr() + 4096,
+                                                    int(need.value), st))
+                    w = ws.cpu().numpy()
+                    assert np.all(w[:4096] == 0x5A) and np.all(w[4096 + int(need.value):] == 0x5A)
+                if op != 1:
+                    sc = np.array([3], dtype=dt)
+                    _native.check(L.exsum_elementwise(ptr, None, sc.ctypes.data, dcode, op, m, 2, n,
+                                                      st))
+                _native.check(L.exsum_elementwise(ptr, ptr, None, dcode, op, m, 0, n, st))
+                res = torch.zeros(2, dtype=buf.dtype, device="cuda")
+                fws = torch.empty(int(L.exsum_fold_workspace_bytes()), dtype=torch.uint8,
+                                  device="cuda")
+                _native.check(L.exsum_fold(ptr, res.data_ptr(), dcode, op, m, n, fws.data_ptr(),
+                                           fws.numel(), st))
+                torch.cuda.synchronize()
+                h = buf.cpu().numpy()
+                assert np.array_equal(h[:GUARD + shift].view(np.uint8),
+                                      np.zeros(GUARD + shift, dt).view(np.uint8))
+                assert np.array_equal(h[GUARD + shift + n:].view(np.uint8),
+                                      np.zeros(len(h) - GUARD - shift - n, dt).view(np.uint8))
+                assert res[1].item() == 0  # fold writes exactly one element
+
+
+def test_concurrent_calls_on_separate_streams(ex):
+    """Several host threads, one stream each, different routes at once: same
+    results as one at a time (host caches, smem-limit cache and the launch
+    counters are thread-safe; ctypes releases the GIL)."""
+    import threading
+
+    import torch
+
+    rng = np.random.default_rng(33)
+    jobs = []
+    for i in range(6):
+        shape = [(48, 40, 256), (30, 64, 512), (200, 300), (16, 17, 1024), (9, 8, 7, 6), (500,)][i]
+        box = [(8, 8, 8), (4, 4, 4), (16, 16), (16, 16, 16), (2, 3, 4, 5), (33,)][i]
+        a = torch.from_numpy(rng.standard_normal(shape).astype(np.float32)).cuda()
+        route = ["box-complement", "bdbsc", "sat", "bdbs", "box-complement", "bdbs"][i]
+        jobs.append((route, a, box))
+    fns = {"bdbs": ex.bdbs_included, "bdbsc": ex.bdbs_excluded,
+           "box-complement": ex.box_complement_excluded, "sat": ex.sat_included}
+    want = [fns[r](ex.Tensor(ex.Float32AddOps(), a), box).data.clone() for r, a, box in jobs]
+    torch.cuda.synchronize()
+    got = [None] * len(jobs)
+    errors = []
+
+    def work(i):
+        try:
+            s = torch.cuda.Stream()
+            r, a, box = jobs[i]
+            with torch.cuda.stream(s):
+                for _ in range(5):
+                    got[i] = fns[r](ex.Tensor(ex.Float32AddOps(), a), box).data
+            s.synchronize()
+        except Exception as e:  # pragma: no cover - reported below
+            errors.append(repr(e))
+
+    th = [threading.Thread(target=work, args=(i,)) for i in range(len(jobs))]
+    for t in th:
+        t.start()
+    for t in th:
+        t.join()
+    assert not errors, errors
+    for g, w in zip(got, want):
+        assert torch.equal(g, w)
