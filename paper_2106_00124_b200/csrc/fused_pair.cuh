@@ -272,7 +272,7 @@ k_fused_pair(const T* __restrict__ in, T* __restrict__ out, int64_t outer, int64
           }
           __syncwarp();
           T etail = T(0);
-          if constexpr (ADD_EXCL) etail = tails[ri];
+          if constexpr (ADD_EXCL) etail = OpAdd::apply(rtot, tails[ri]);  // row total + tail
 #pragma unroll
           for (int v = 0; v < CV; ++v) {
             VT q;
@@ -280,7 +280,7 @@ k_fused_pair(const T* __restrict__ in, T* __restrict__ out, int64_t outer, int64
             for (int j = 0; j < VE; ++j) {
               const T w = a[v * VE + j];
               if constexpr (ADD_EXCL) {
-                q.v[j] = Op::apply(OpAdd::inverse<T>(rtot, w), etail);
+                q.v[j] = OpAdd::inverse<T>(etail, w);  // (row total + tail) - window
               } else {
                 q.v[j] = epi ? OpAdd::inverse<T>(tot, w) : w;
               }
