@@ -14,6 +14,8 @@
 // next block's prefix streams from its stage, and results go straight to
 // global memory (32 lanes x 8 bytes = one coalesced row per store).  Registers
 // are O(1) in k; the ring keeps R-1 blocks of loads in flight per warp.
+#include <stdlib.h>
+
 #include "exsum_common.cuh"
 #include "exsum_launch.h"
 
@@ -139,8 +141,12 @@ template <class T, class Op>
 int go_bulk(const T* in, T* out, int64_t outer, int64_t n, int64_t inner, int64_t k,
             const typename AccOf<T>::type* total, cudaStream_t s) {
   const size_t stage = (size_t)k * 32 * sizeof(T);
-  int R = 4;
-  while (R > 2 && 128 + R * stage > 100 * 1024) --R;
+  // two stages (the block being stitched + the next block in flight): more
+  // resident warps beat deeper per-warp prefetch (C5 f64: k=32 0.83 -> 0.71 ms,
+  // k=128 1.20 -> 0.92 ms for R = 4/3 -> 2)
+  int R = 2;
+  static const char* rs = getenv("EXSUM_BULK_R");  // measurement override
+  if (rs && atoi(rs) >= 2 && atoi(rs) <= 6) R = atoi(rs);
   const size_t smem = 128 + R * stage;
   if (smem > 200 * 1024) return -1;
   const int64_t strips = inner / 32;

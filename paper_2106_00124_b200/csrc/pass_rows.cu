@@ -388,6 +388,7 @@ template <class T, class Op, int W, int WARPS>
 __global__ void __launch_bounds__(WARPS * 32)
 k_rows_suffix(const T* __restrict__ in, T* __restrict__ out, int64_t rows, int64_t n,
               const typename AccOf<T>::type* __restrict__ total) {
+  static_assert(W == 32, "one chunk column per lane");
   constexpr int STRIDE = W + 1;
   __shared__ T smem[WARPS][32 * STRIDE];
   const int lane = threadIdx.x & 31;
@@ -400,13 +401,28 @@ k_rows_suffix(const T* __restrict__ in, T* __restrict__ out, int64_t rows, int64
   for (int64_t g = warp; g < groups; g += nwarps) {
     const int64_t r0 = g * 32;
     const int nr = rows - r0 >= 32 ? 32 : (int)(rows - r0);
+    // chunks of W columns from the row end; 32 independent loads per chunk,
+    // the next chunk's loads issued while the current one is scanned
+    T v[32];
+    {
+      const int64_t xs = n - W > 0 ? n - W : 0;
+      const int64_t x = xs + lane;
+#pragma unroll
+      for (int r = 0; r < 32; ++r) v[r] = (r < nr && x < n) ? ld1(in + (r0 + r) * n + x) : T(0);
+    }
     T S = T(0);
     for (int64_t xe = n; xe > 0; xe -= W) {
       const int64_t xs = xe - W > 0 ? xe - W : 0;
       const int w = (int)(xe - xs);
-      for (int r = 0; r < nr; ++r)
-        for (int x = lane; x < w; x += 32) sm[r * STRIDE + x] = ld1(in + (r0 + r) * n + xs + x);
+#pragma unroll
+      for (int r = 0; r < 32; ++r) sm[r * STRIDE + lane] = v[r];
       __syncwarp();
+      if (xs > 0) {
+        const int64_t ns = xs - W > 0 ? xs - W : 0;
+        const int64_t x = ns + lane;
+#pragma unroll
+        for (int r = 0; r < 32; ++r) v[r] = (r < nr && x < xs) ? ld1(in + (r0 + r) * n + x) : T(0);
+      }
       if (lane < nr) {
         int x = w - 1;
         if (xe == n) {
@@ -419,10 +435,11 @@ k_rows_suffix(const T* __restrict__ in, T* __restrict__ out, int64_t rows, int64
         }
       }
       __syncwarp();
-      for (int r = 0; r < nr; ++r)
-        for (int x = lane; x < w; x += 32) {
-          const T v = sm[r * STRIDE + x];
-          st1(out + (r0 + r) * n + xs + x, epi ? OpAdd::inverse<T>(tot, v) : v);
+#pragma unroll
+      for (int r = 0; r < 32; ++r)
+        if (r < nr && lane < w) {
+          const T t = sm[r * STRIDE + lane];
+          st1(out + (r0 + r) * n + xs + lane, epi ? OpAdd::inverse<T>(tot, t) : t);
         }
       __syncwarp();
     }
