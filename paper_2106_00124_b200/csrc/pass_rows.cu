@@ -308,18 +308,41 @@ k_rows_tile(const T* __restrict__ in, T* __restrict__ out, int64_t rows, int64_t
   const int64_t nchunks = rows * cpr;
   const int64_t ntiles = (nchunks + 31) / 32;
 
+  // each lane's share of a tile's 16-byte vectors, held in registers so the
+  // next tile's loads are in flight while this one is computed
+  constexpr int PV = (33 * CVMAX + 31) / 32;
+  // wide chunks (CVMAX > 8, e.g. f64 k = 32) would hold two chunks of
+  // registers at once: they load each tile right before staging it instead
+  constexpr bool PREFETCH = CVMAX <= 8;
+  VT pre[PV];
+  auto load_tile = [&](int64_t t) {
+    if (t >= ntiles) return;
+    const int64_t a0 = nchunks - t * 32;
+    const int nl = a0 >= 33 ? 33 : (int)a0;
+    const VT* src = reinterpret_cast<const VT*>(in + t * 32 * C);
+#pragma unroll
+    for (int i = 0; i < PV; ++i) {
+      const int v = lane + 32 * i;
+      if (v < nl * CV) pre[i] = ld_stream<T, VE>(reinterpret_cast<const T*>(src + v));
+    }
+  };
+  if (PREFETCH) load_tile(warp);
+
   for (int64_t tile = warp; tile < ntiles; tile += nwarps) {
     const int64_t c0 = tile * 32;
     const int64_t avail = nchunks - c0;  // chunks left from c0 (>= 1)
     const int nload = avail >= 33 ? 33 : (int)avail;
-    const VT* src = reinterpret_cast<const VT*>(in + c0 * C);
-#pragma unroll 4
-    for (int v = lane; v < nload * CV; v += 32) {
-      const VT q = ld_stream<T, VE>(reinterpret_cast<const T*>(src + v));
-      const int cq = (int)(((unsigned)v * cv_magic) >> 16);  // v / CV (v < 4096)
-      *reinterpret_cast<VT*>(sm + cq * STRIDE + (v - cq * CV) * VE) = q;
+    if (!PREFETCH) load_tile(tile);
+#pragma unroll
+    for (int i = 0; i < PV; ++i) {
+      const int v = lane + 32 * i;
+      if (v < nload * CV) {
+        const int cq = (int)(((unsigned)v * cv_magic) >> 16);  // v / CV (v < 4096)
+        *reinterpret_cast<VT*>(sm + cq * STRIDE + (v - cq * CV) * VE) = pre[i];
+      }
     }
     __syncwarp();
+    if (PREFETCH) load_tile(tile + nwarps);
     const int64_t c = c0 + lane;
     const bool valid = lane < nload && lane < 32 && c < nchunks;
     const int64_t xc = valid ? (c % cpr) * C : 0;  // chunk start within its row
