@@ -48,7 +48,8 @@ namespace exsum {
 // (C <= 8: 64-thread CTAs whose shared ring and stage bound the CTAs per SM)
 // take 8-row units where K1 allows, doubling the resident CTAs.
 __host__ __device__ constexpr int fp_unit_rows(int C, int K1) {
-  return (C <= FP_NARROW_C && K1 <= 8) ? 8 : (16 / K1 > 0 ? 16 / K1 : 1) * K1;
+  return (C <= FP_NARROW_C && K1 <= 4) ? 4 : (C <= FP_NARROW_C && K1 <= 8) ? 8
+                                                : (16 / K1 > 0 ? 16 / K1 : 1) * K1;
 }
 
 template <class T, class Op, int C, int K1, int MODE, int TV>
