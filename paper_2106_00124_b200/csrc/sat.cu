@@ -423,7 +423,9 @@ k_sat_query_rows(const T* __restrict__ S, T* __restrict__ out, QShape q, int64_t
 #pragma unroll
       for (int pp = 0; pp < NP; ++pp) {
         const bool valid = (vmask >> pp) & 1;
-        const bool par = (par_mask >> pp) & 1;
+        // sign of the term: the parity of its low picks, a compile-time
+        // constant of the unrolled pattern index (no per-element select)
+        const bool par = __popc((unsigned)pp) & 1;
         const T h = __ldg(src[pp] + hi);
         const T l = __ldg(src[pp] + lo);
         const T vh = valid ? h : T(0);
@@ -468,7 +470,7 @@ k_sat_query_rows(const T* __restrict__ S, T* __restrict__ out, QShape q, int64_t
 // row-at-a-time form.  A 4-slot cp.async ring keeps two steps of prefetch in
 // flight (Little's law: ~64 KB per SM at HBM latency).  A work item (chain) is (the other leading coordinates, r); chains
 // are ordered so that CTAs running together share S planes in L2.
-template <class T, int DH>
+template <class T, int DH, int NT>
 __global__ void __launch_bounds__(256)
 k_sat_query_chain(const T* __restrict__ S, T* __restrict__ out, QShape q, int64_t chains,
                   const typename AccOf<T>::type* __restrict__ total, int mode, FastMod fm) {
@@ -477,7 +479,9 @@ k_sat_query_chain(const T* __restrict__ S, T* __restrict__ out, QShape q, int64_
   constexpr int VE = 16 / sizeof(T);
   extern __shared__ __align__(16) unsigned char smem_raw[];
   T* buf = reinterpret_cast<T*>(smem_raw);
-  const int n = (int)q.ext[DH];
+  // NT > 0: the row length at compile time, so the per-pattern row offsets
+  // below are immediates of the shared loads (no per-load address math)
+  const int n = NT > 0 ? NT : (int)q.ext[DH];
   const int kl = (int)q.k[DH];
   const int pitch = n + VE;
   const int slot_elems = NQ * pitch;
@@ -576,18 +580,23 @@ k_sat_query_chain(const T* __restrict__ S, T* __restrict__ out, QShape q, int64_
       const T* lob = buf + (size_t)lo_slot * slot_elems;
       const T* hib = buf + (size_t)hi_slot * slot_elems;
       T* dst = out + obase_lead + xc * strc;
+      const int xmain = n - kl + 1;  // x < xmain: the high corner x + kl - 1 is in the row
       for (int x = tid; x < n; x += 256) {
-        const int hi = VE + (x + kl - 1 < n - 1 ? x + kl - 1 : n - 1);
+        const int hi = VE + (x < xmain ? x + kl - 1 : n - 1);
         const int lo = VE - 1 + x;  // x - 1; the zero pad for x = 0
+        // four base addresses; every pattern's row is a constant offset from one
+        const T* lh = lob + hi;
+        const T* ll = lob + lo;
+        const T* hh = hib + hi;
+        const T* hl = hib + lo;
         T acc = T(0);
 #pragma unroll
         for (int pp = 0; pp < 2 * NQ; ++pp) {
           const int qq = pp >> 1;
           const bool clo = pp & 1;  // chain axis takes its low corner
-          const bool par = (((qpar >> qq) & 1) ^ (int)clo) != 0;
-          const T* rb = (clo ? lob : hib) + qq * pitch;
-          const T vh = rb[hi];
-          const T vl = rb[lo];
+          const bool par = ((__popc((unsigned)qq) + (int)clo) & 1) != 0;  // compile-time
+          const T vh = (clo ? lh : hh)[qq * pitch];
+          const T vl = (clo ? ll : hl)[qq * pitch];
           if (pp == 0) {
             acc = vh;  // the all-high corner is copied (included.py:116-117)
           } else {
@@ -707,11 +716,17 @@ int go_query(const T* S, T* out, const QShape& q, int64_t N, const void* total, 
       const int per_sm = smem <= 50 * 1024 ? 4 : smem <= 64 * 1024 ? 3 : 2;
       const int64_t cap = (int64_t)num_sms() * per_sm;
       const unsigned gr = (unsigned)(chains < cap ? chains : cap);
-#define EXSUM_CHAIN(DH)                                                                        \
+#define EXSUM_CHAIN_N(DH, NT)                                                                  \
   {                                                                                            \
-    auto kfn = k_sat_query_chain<T, DH>;                                                       \
+    auto kfn = k_sat_query_chain<T, DH, NT>;                                                   \
     ensure_smem((const void*)kfn, smem);                                                       \
     kfn<<<gr, 256, smem, s>>>(S, out, q, chains, tot, mode, fm);                               \
+  }
+#define EXSUM_CHAIN(DH)                                                                        \
+  {                                                                                            \
+    if (n == 512) EXSUM_CHAIN_N(DH, 512)                                                       \
+    else if (n == 1024) EXSUM_CHAIN_N(DH, 1024)                                                \
+    else EXSUM_CHAIN_N(DH, 0)                                                                  \
   }
       switch (q.d) {
         case 2: EXSUM_CHAIN(1) break;
@@ -721,6 +736,7 @@ int go_query(const T* S, T* out, const QShape& q, int64_t N, const void* total, 
         case 6: EXSUM_CHAIN(5) break;
       }
 #undef EXSUM_CHAIN
+#undef EXSUM_CHAIN_N
       return 1;
     }
   }
