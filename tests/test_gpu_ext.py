@@ -237,3 +237,28 @@ def test_run_many_host_batch_matches_single_calls(ex):
     with pytest.raises(ex.UsageError):
         ex.run_many("bdbs", [ex.Tensor(ex.IntAddOps(), np.zeros((3, 4), dtype=np.int64)),
                              ex.Tensor(ex.IntAddOps(), np.zeros((4, 3), dtype=np.int64))], (2, 2))
+
+
+@pytest.mark.parametrize("d", [7, 9, 12])
+def test_high_dimensional_routes(ex, d):
+    """d up to 12 (the generic kernels: box-complement's recursive tail, the
+    2^d-term SAT query), every dtype/operator, against the oracle."""
+    rng = np.random.default_rng(40 + d)
+    shape = tuple(int(v) for v in rng.integers(1, 4, size=d))
+    while int(np.prod(shape)) < 64:
+        shape = tuple(int(v) for v in rng.integers(1, 4, size=d))
+    box = tuple(int(v) for v in rng.integers(1, 4, size=d))
+    for mono in ("add-i64", "max-i64", "add-f64", "mod-add:13"):
+        a = (rng.standard_normal(shape) if mono == "add-f64"
+             else rng.integers(-50, 50, size=shape, dtype=np.int64))
+        op = mono_op(mono)
+        routes = ["bdbs", "box-complement"] + ([] if mono == "max-i64" else ["bdbsc", "sat", "satc"])
+        for route in routes:
+            got = _run(ex, route, mono, a, box)
+            want = orc.ROUTES[route](a, box, op)
+            if a.dtype.kind == "f" and route != "bdbs" and route != "sat":
+                k = tuple(min(b, e) for b, e in zip(box, shape))
+                ok, ratio, rel = compare(route, got, float64_oracle(route, a, k, orc), a, k, orc)
+                assert ok, (d, route, ratio)
+            else:
+                assert _bits_equal(got, want), (d, mono, route, shape, box)
