@@ -69,6 +69,43 @@ def _rewrap(t, out):
         return Tensor(t.ops, out)
 
 
+# per-call constants of a (route, dtype, op, extents, box, modulus) combination:
+# the workspace size and the ctypes argument arrays (small calls are host-bound)
+_PLAN_CACHE: dict = {}
+# one growing workspace per (device, stream): work on a stream is ordered, so a
+# call may reuse the buffer the previous call on the same stream used
+_WS_CACHE: dict = {}
+
+
+def _plan(route, dtype, op, ext, k, modulus):
+    key = (route, dtype, op, ext, k, modulus)
+    p = _PLAN_CACHE.get(key)
+    if p is None:
+        p = (_native.workspace_bytes(route, dtype, op, ext, k, modulus),
+             _native.i64_array(ext), _native.i64_array(k))
+        if len(_PLAN_CACHE) > 4096:
+            _PLAN_CACHE.clear()
+        _PLAN_CACHE[key] = p
+    return p
+
+
+def _workspace(device, stream, nbytes):
+    import torch
+
+    key = (device.index, stream)
+    ws = _WS_CACHE.get(key)
+    if ws is None or ws.numel() < nbytes:
+        ws = torch.empty(max(nbytes, 1), dtype=torch.uint8, device=device)
+        _WS_CACHE[key] = ws
+    return ws
+
+
+def release_workspace_cache() -> None:
+    """Drop the cached per-stream workspaces (and the library's host-path buffers)."""
+    _WS_CACHE.clear()
+    _native.load().exsum_release_cache()
+
+
 def run_device(route: str, x, dtype: str, op: str, ext, k, out=None, modulus: int = 0):
     """Run ``route`` on a CUDA torch tensor; returns the output tensor.
     ``modulus``: m of a ``mod-add:<m>`` operator (op == "mod-add")."""
@@ -84,14 +121,14 @@ def run_device(route: str, x, dtype: str, op: str, ext, k, out=None, modulus: in
     elif out.data_ptr() % 16 or not out.is_contiguous():
         raise UsageError("out must be a contiguous, 16-byte aligned CUDA tensor")
     L = _native.load()
-    ws_bytes = _native.workspace_bytes(route, dtype, op, ext, k, modulus)
+    ext, k = tuple(ext), tuple(k)
+    ws_bytes, c_ext, c_k = _plan(route, dtype, op, ext, k, int(modulus))
     with torch.cuda.device(x.device):
-        ws = torch.empty(max(ws_bytes, 1), dtype=torch.uint8, device=x.device)
         stream = torch.cuda.current_stream(x.device).cuda_stream
+        ws = _workspace(x.device, stream, ws_bytes)
         _native.check(L.exsum_route(_native.ROUTE[route], x.data_ptr(), out.data_ptr(),
                                     _native.DTYPE[dtype], _native.OP[op], int(modulus), len(ext),
-                                    _native.i64_array(ext), _native.i64_array(k), ws.data_ptr(),
-                                    ws_bytes, stream))
+                                    c_ext, c_k, ws.data_ptr(), ws_bytes, stream))
     return out
 
 
