@@ -219,8 +219,9 @@ class DistComm:
             ops.append(dist.P2POp(dist.irecv, recv, src))
         if not ops:
             return []
-        if self.nccl:
-            return list(dist.batch_isend_irecv(ops))
+        # plain non-blocking isend / irecv on every backend: the gloo tests run
+        # exactly this code, and unlike batch_isend_irecv it has no requirement
+        # that every rank take part in the first batch (a rank may own no planes)
         return [(dist.isend if o.op is dist.isend else dist.irecv)(o.tensor, o.peer) for o in ops]
 
     def all_gather_rows(self, t, counts):
