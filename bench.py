@@ -203,12 +203,26 @@ def run_reference(args, rank, world):
         "config": {"workload": cfg, "description": desc, "extents": list(ext), "box": list(box),
                    "route": args.route},
         "cpu_baseline": {"value": value, "unit": UNIT, "cores": nthreads, "kind": "port",
+                         "cpu_model": _cpu_model(), "cpu_count": os.cpu_count(),
                          "sample": f"{args.route} on the first {shape[0]} planes "
                                    f"({'x'.join(map(str, shape))}) of the workload, "
                                    f"oracle/exsum_oracle.c with {nthreads} OpenMP threads"},
         "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
     }
     print(json.dumps(line), flush=True)
+
+
+def _cpu_model():
+    """The host CPU's model string (report it beside the core count)."""
+    try:
+        for line in open("/proc/cpuinfo"):
+            if line.lower().startswith("model name"):
+                return line.split(":", 1)[1].strip()
+    except OSError:
+        pass
+    import platform
+
+    return platform.processor() or "unknown"
 
 
 def _dt(dtype):
@@ -460,6 +474,7 @@ def main():
         nthreads = os.cpu_count() or 1
         v, shape, dt = cpu_sample(args.config, args.route, nthreads, planes=args.cpu_planes)
         cpu = {"value": v, "unit": UNIT, "cores": nthreads, "kind": "port",
+               "cpu_model": _cpu_model(), "cpu_count": os.cpu_count(),
                "sample": f"{args.route} on the first {shape[0]} planes ({'x'.join(map(str, shape))}) "
                          f"of the workload, oracle/exsum_oracle.c, {nthreads} OpenMP threads, "
                          f"{dt:.2f} s"}
