@@ -20,12 +20,7 @@ int go_axis_stream_c(const T* in, T* out, int64_t outer, int64_t n, int64_t inne
   const int64_t strips = inner / N2;
   const int64_t lines = outer * strips;
   const int64_t nunits = (nout + U - 1) / U;
-  const int64_t want = (int64_t)num_sms() * per_sm * 3;
-  int64_t nseg = (want + lines - 1) / lines;
-  int64_t max_seg = nunits / 4;
-  if (max_seg < 1) max_seg = 1;
-  if (nseg > max_seg) nseg = max_seg;
-  if (nseg < 1) nseg = 1;
+  int64_t nseg = pick_segments(lines, nunits, per_sm);
   const int64_t seg_len = U * ((nunits + nseg - 1) / nseg);
   nseg = (nout + seg_len - 1) / seg_len;
   const int64_t items = lines * nseg;

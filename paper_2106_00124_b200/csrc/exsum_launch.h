@@ -161,4 +161,34 @@ int launch_fold_result(int dtype, int op, const FastMod& fm, const void* acc, vo
 size_t dtype_size(int dtype);
 int num_sms();
 
+// Segments per line for the streaming kernels (one CTA streams one (line,
+// segment) item of `nunits` units).  With one resident CTA per SM the count
+// minimises (waves of items, rounded up) x (units per item + 1 for the halo
+// block and pipeline fill): a whole extra wave for a few leftover items costs
+// more than a short halo (C5 f64: 512 single-line items on 148 SMs were 3.46
+// waves).  Smaller CTAs keep ~3 waves of items so several stay resident per SM.
+inline int64_t pick_segments(int64_t lines, int64_t nunits, int per_sm) {
+  int64_t max_seg = nunits / 4;
+  if (max_seg < 1) max_seg = 1;
+  const int64_t slots = (int64_t)num_sms() * per_sm;
+  if (per_sm > 1) {
+    int64_t nseg = (slots * 3 + lines - 1) / lines;
+    if (nseg > max_seg) nseg = max_seg;
+    return nseg < 1 ? 1 : nseg;
+  }
+  if (max_seg > 64) max_seg = 64;
+  int64_t nseg = 1;
+  double best = 1e300;
+  for (int64_t c = 1; c <= max_seg; ++c) {
+    const int64_t per = (nunits + c - 1) / c;
+    const int64_t items = lines * ((nunits + per - 1) / per);
+    const double cost = (double)((items + slots - 1) / slots) * ((double)per + 1.0);
+    if (cost < best * 0.999) {
+      best = cost;
+      nseg = c;
+    }
+  }
+  return nseg;
+}
+
 }  // namespace exsum

@@ -438,13 +438,8 @@ int go_pair(const T* in, T* out, int64_t outer, int64_t n1, int64_t kx,
   if (per_sm > 2048 / NT) per_sm = 2048 / NT;
   if (per_sm < 1) per_sm = 1;
   const int64_t nunits = (n1 + U - 1) / U;
-  // enough CTAs for ~3 waves of resident CTAs; segments keep >= 4 units
-  const int64_t want = (int64_t)num_sms() * per_sm * 3;
-  int64_t nseg = (want + outer - 1) / outer;
-  int64_t max_seg = nunits / 4;
-  if (max_seg < 1) max_seg = 1;
-  if (nseg > max_seg) nseg = max_seg;
-  if (nseg < 1) nseg = 1;
+  // segments per outer index (exsum_launch.h: wave rounding vs halo + fill)
+  int64_t nseg = pick_segments(outer, nunits, per_sm);
   const int64_t seg_len = U * ((nunits + nseg - 1) / nseg);
   nseg = (n1 + seg_len - 1) / seg_len;
   const int64_t items = outer * nseg;
