@@ -53,10 +53,11 @@ __host__ __device__ constexpr int fp_unit_rows(int C, int K1) {
 }
 
 template <class T, class Op, int C, int K1, int MODE, int TV>
-// narrow 4-byte rows (64-thread CTAs) ask for 12 resident CTAs: a register cap
-// that raises the warps per SM there (C3b 0.033 -> 0.030 ms); 8-byte ones
-// (128 threads) would spill under it
-__global__ void __launch_bounds__(32 * C / TV, (C <= 8 && sizeof(T) == 4 ? 12 : 1))
+// narrow rows ask for more resident CTAs: a register cap that raises the warps
+// per SM there (4-byte, 64-thread CTAs: 12, C3b 0.033 -> 0.030 ms; 8-byte,
+// 128 threads: 4, C2 0.066 -> 0.062 ms, except the max row op, which spills)
+__global__ void __launch_bounds__(32 * C / TV,
+                                   (C <= 8 ? (sizeof(T) == 4 ? 12 : (MODE == ROW_EXCL ? 1 : 4)) : 1))
 k_fused_pair(const T* __restrict__ in, T* __restrict__ out, int64_t outer, int64_t n1,
              int64_t kx, int64_t seg_len, int64_t nseg,
              const typename AccOf<T>::type* __restrict__ total, const T* __restrict__ Tail) {
