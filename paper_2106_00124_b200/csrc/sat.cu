@@ -39,10 +39,12 @@ namespace exsum {
 // Inclusive running sum along the contiguous axis of [rows, n], in segments
 // of L (nseg per row; nseg == 1: whole rows).  Work item = (row, segment);
 // 32 items per warp, one per lane, staged through a padded 32x33 tile.
-template <class T, class Op, int WARPS>
+template <class T, class Op, int WARPS, int W>
 __global__ void __launch_bounds__(WARPS * 32)
 k_scan_rows(const T* in, T* out, int64_t rows, int64_t n, int64_t L, int64_t nseg, int rev) {
-  constexpr int W = 32;
+  // W elements of each of 32 lines per chunk: CPL = W / 32 per lane and line
+  // (4-byte types take 64: 256-byte runs per line and fetch)
+  constexpr int CPL = W / 32;
   constexpr int STRIDE = W + 1;
   __shared__ T smem[WARPS][32 * STRIDE];
   __shared__ int64_t sbase[WARPS][32], slen[WARPS][32];
@@ -75,25 +77,32 @@ k_scan_rows(const T* in, T* out, int64_t rows, int64_t n, int64_t L, int64_t nse
     }
     __syncwarp();
     T acc = T(0);
-    // 32 independent loads per chunk; the next chunk's loads are issued as soon
-    // as the current one is staged, so they overlap its scan and stores
-    T v[32];
+    // 32 * CPL independent loads per chunk; the next chunk's loads are issued
+    // as soon as the current one is staged, so they overlap its scan and stores
+    T v[32 * CPL];
 #pragma unroll
-    for (int r = 0; r < 32; ++r) {
-      const int64_t l = slen[wid][r];
-      v[r] = lane < l ? ld1(in + sbase[wid][r] + dir * lane) : T(0);
-    }
+    for (int r = 0; r < 32; ++r)
+#pragma unroll
+      for (int c = 0; c < CPL; ++c) {
+        const int64_t l = slen[wid][r];
+        const int x = c * 32 + lane;
+        v[r * CPL + c] = x < l ? ld1(in + sbase[wid][r] + dir * x) : T(0);
+      }
     for (int64_t xo = 0; xo < maxlen; xo += W) {
 #pragma unroll
-      for (int r = 0; r < 32; ++r) sm[r * STRIDE + lane] = v[r];
+      for (int r = 0; r < 32; ++r)
+#pragma unroll
+        for (int c = 0; c < CPL; ++c) sm[r * STRIDE + c * 32 + lane] = v[r * CPL + c];
       __syncwarp();
       if (xo + W < maxlen) {
-        const int64_t xn = xo + W + lane;
 #pragma unroll
-        for (int r = 0; r < 32; ++r) {
-          const int64_t l = slen[wid][r];
-          v[r] = xn < l ? ld1(in + sbase[wid][r] + dir * xn) : T(0);
-        }
+        for (int r = 0; r < 32; ++r)
+#pragma unroll
+          for (int c = 0; c < CPL; ++c) {
+            const int64_t l = slen[wid][r];
+            const int64_t xn = xo + W + c * 32 + lane;
+            v[r * CPL + c] = xn < l ? ld1(in + sbase[wid][r] + dir * xn) : T(0);
+          }
       }
       if (mylen > xo) {
         const int w = mylen - xo < W ? (int)(mylen - xo) : W;
@@ -114,10 +123,13 @@ k_scan_rows(const T* in, T* out, int64_t rows, int64_t n, int64_t L, int64_t nse
       }
       __syncwarp();
 #pragma unroll
-      for (int r = 0; r < 32; ++r) {
-        const int64_t l = slen[wid][r];
-        if (xo + lane < l) st1(out + sbase[wid][r] + dir * (xo + lane), sm[r * STRIDE + lane]);
-      }
+      for (int r = 0; r < 32; ++r)
+#pragma unroll
+        for (int c = 0; c < CPL; ++c) {
+          const int64_t l = slen[wid][r];
+          const int64_t x = xo + c * 32 + lane;
+          if (x < l) st1(out + sbase[wid][r] + dir * x, sm[r * STRIDE + c * 32 + lane]);
+        }
       __syncwarp();
     }
   }
@@ -679,8 +691,13 @@ int go_scan(const T* in, T* out, int64_t outer, int64_t n, int64_t inner, int64_
   if (inner == 1) {
     constexpr int WARPS = 4;
     const int64_t groups = (outer * nseg + 31) / 32;
-    k_scan_rows<T, Op, WARPS><<<(unsigned)grid_for(groups * 32, WARPS * 32, 16), WARPS * 32, 0,
-                                s>>>(in, out, outer, n, L, nseg, rev);
+    if constexpr (sizeof(T) == 4) {
+      k_scan_rows<T, Op, WARPS, 64><<<(unsigned)grid_for(groups * 32, WARPS * 32, 16),
+                                      WARPS * 32, 0, s>>>(in, out, outer, n, L, nseg, rev);
+    } else {
+      k_scan_rows<T, Op, WARPS, 32><<<(unsigned)grid_for(groups * 32, WARPS * 32, 16),
+                                      WARPS * 32, 0, s>>>(in, out, outer, n, L, nseg, rev);
+    }
     return 1;
   }
   constexpr int VE = 16 / sizeof(T);
