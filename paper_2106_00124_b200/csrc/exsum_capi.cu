@@ -935,6 +935,121 @@ int exsum_windowed_pass(const void* in, void* out, int dtype, int op, int d, con
   return cuda_check("kernel launch");
 }
 
+// BDBS on host buffers, pipelined over axis-0 chunks: output planes depend only
+// on input planes [x0, x0 + k0 - 1], so chunk j (a multiple of k0 planes) runs
+// the axis-0 shard stage (its halo is chunk j+1's first k0-1 planes, already in
+// the device copy) and the finish stage while chunk j+1 is copied in and chunk
+// j-1 is copied out -- the copy engines run both directions at once.  Block-
+// aligned chunks keep the reference's association: bit-identical to one call.
+static int bdbs_host_pipelined(const Shape& s, const int64_t* box, const void* h_in, void* h_out,
+                        int dtype, int op) {
+  const size_t es = dtype_size(dtype);
+  const int d = s.d;
+  const int64_t n0 = s.ext[0], k0 = s.k[0];
+  const int64_t plane = s.N / n0;
+  int64_t P = (n0 + 15) / 16;  // ~16 chunks: the unoverlapped first H2D / last D2H is 1/16
+  P = (P + k0 - 1) / k0 * k0;
+  const int64_t nch = (n0 + P - 1) / P;
+  int64_t ext_c[EXSUM_MAX_DIMS];
+  for (int i = 0; i < d; ++i) ext_c[i] = s.ext[i];
+  // workspace: the axis-0 stage output (P planes) + the larger stage workspace
+  size_t ws0 = 0, ws1 = 0;
+  {
+    ext_c[0] = P + (k0 - 1 < n0 - P ? k0 - 1 : (n0 - P > 0 ? n0 - P : 0));
+    Arena a0(nullptr);
+    int l = 0;
+    int rc = run_stage(0, dtype, op, d, ext_c, box, P, 0, (const void*)256, (void*)512, nullptr,
+                       nullptr, a0, nullptr, &l);
+    if (rc) return rc;
+    ws0 = a0.off;
+    ext_c[0] = P;
+    Arena a1(nullptr);
+    rc = run_stage(1, dtype, op, d, ext_c, box, 0, 0, (const void*)256, (void*)512, nullptr,
+                   nullptr, a1, nullptr, &l);
+    if (rc) return rc;
+    ws1 = a1.off;
+  }
+  int dev = 0;
+  if (cudaGetDevice(&dev) != cudaSuccess) return cuda_check("cudaGetDevice");
+  BatchCache& c = batch_cache();
+  std::lock_guard<std::mutex> lock(c.mu);
+  size_t di = 0;
+  while (di < c.dev.size() && c.dev[di] != dev) ++di;
+  if (di == c.dev.size()) {
+    c.dev.push_back(dev);
+    for (int k = 0; k < 2; ++k) {
+      BatchSlot b;
+      if (cudaEventCreateWithFlags(&b.h2d, cudaEventDisableTiming) != cudaSuccess ||
+          cudaEventCreateWithFlags(&b.done, cudaEventDisableTiming) != cudaSuccess ||
+          cudaEventCreateWithFlags(&b.d2h, cudaEventDisableTiming) != cudaSuccess)
+        return cuda_check("cudaEventCreate");
+      c.slots.push_back(b);
+    }
+    for (int k = 0; k < 3; ++k) {
+      cudaStream_t st;
+      if (cudaStreamCreateWithFlags(&st, cudaStreamNonBlocking) != cudaSuccess)
+        return cuda_check("cudaStreamCreate");
+      c.streams.push_back(st);
+    }
+  }
+  // buffers: slot 0 holds the whole input and output; slot 1's `in` the stage
+  // output, its `ws` the stage workspace
+  BatchSlot* slot = &c.slots[2 * di];
+  const size_t bytes = (size_t)s.N * es;
+  const size_t ybytes = (size_t)(P * plane) * es;
+  const size_t wsb = (ws0 > ws1 ? ws0 : ws1) > 0 ? (ws0 > ws1 ? ws0 : ws1) : 256;
+  if (slot[0].in.reserve(bytes) || slot[0].out.reserve(bytes) || slot[1].in.reserve(ybytes) ||
+      slot[1].ws.reserve(wsb))
+    return fail(EXSUM_ECUDA, "cudaMalloc failed for the pipelined host path");
+  cudaStream_t s_in = c.streams[3 * di], s_run = c.streams[3 * di + 1], s_out = c.streams[3 * di + 2];
+  std::vector<cudaEvent_t> ev(3 * nch);
+  for (auto& e : ev)
+    if (cudaEventCreateWithFlags(&e, cudaEventDisableTiming) != cudaSuccess)
+      return cuda_check("cudaEventCreate");
+  char* din = (char*)slot[0].in.p;
+  char* dout = (char*)slot[0].out.p;
+  for (int64_t j = 0; j < nch; ++j) {
+    const int64_t a = j * P, b = a + P < n0 ? a + P : n0;
+    cudaMemcpyAsync(din + a * plane * es, (const char*)h_in + a * plane * es,
+                    (size_t)((b - a) * plane) * es, cudaMemcpyHostToDevice, s_in);
+    cudaEventRecord(ev[3 * j], s_in);
+  }
+  int rc = EXSUM_OK;
+  for (int64_t j = 0; j < nch && rc == EXSUM_OK; ++j) {
+    const int64_t a = j * P, b = a + P < n0 ? a + P : n0;
+    const int64_t own = b - a;
+    const int64_t halo = k0 - 1 < n0 - b ? k0 - 1 : n0 - b;
+    cudaStreamWaitEvent(s_run, ev[3 * j], 0);
+    if (halo > 0) cudaStreamWaitEvent(s_run, ev[3 * (j + 1)], 0);
+    if (j >= 1) cudaStreamWaitEvent(s_run, ev[3 * (j - 1) + 1], 0);  // y / ws reuse (same stream)
+    ext_c[0] = own + halo;
+    int l = 0;
+    if (k0 > 1) {
+      Arena ar(slot[1].ws.p);
+      rc = run_stage(0, dtype, op, d, ext_c, box, own, 0, din + a * plane * es, slot[1].in.p,
+                     nullptr, nullptr, ar, s_run, &l);
+      if (rc) break;
+    }
+    ext_c[0] = own;
+    Arena ar1(slot[1].ws.p);
+    rc = run_stage(1, dtype, op, d, ext_c, box, 0, 0, k0 > 1 ? slot[1].in.p : din + a * plane * es,
+                   dout + a * plane * es, nullptr, nullptr, ar1, s_run, &l);
+    g_total_launches += l;
+    cudaEventRecord(ev[3 * j + 1], s_run);
+    cudaStreamWaitEvent(s_out, ev[3 * j + 1], 0);
+    cudaMemcpyAsync((char*)h_out + a * plane * es, dout + a * plane * es,
+                    (size_t)(own * plane) * es, cudaMemcpyDeviceToHost, s_out);
+  }
+  cudaError_t e1 = cudaStreamSynchronize(s_in);
+  cudaError_t e2 = cudaStreamSynchronize(s_run);
+  cudaError_t e3 = cudaStreamSynchronize(s_out);
+  for (auto& e : ev) cudaEventDestroy(e);
+  if (rc) return rc;
+  if (e1 != cudaSuccess || e2 != cudaSuccess || e3 != cudaSuccess)
+    return cuda_check("pipelined host path");
+  return cuda_check("pipelined host path");
+}
+
 int exsum_route_host(int route, const void* h_in, void* h_out, int dtype, int op, int64_t modulus,
                      int d, const int64_t* ext, const int64_t* box) {
   g_err.clear();
@@ -942,6 +1057,13 @@ int exsum_route_host(int route, const void* h_in, void* h_out, int dtype, int op
   int rc = validate(route, dtype, op, modulus, d, ext, box, &s);
   if (rc) return rc;
   if (!h_in || !h_out) return fail(EXSUM_EUSAGE, "null host pointer");
+  if (route == EXSUM_ROUTE_BDBS && op != EXSUM_MODADD && d >= 2 &&
+      (size_t)s.N * dtype_size(dtype) >= ((size_t)64 << 20) && s.ext[0] >= 4 * s.k[0] &&
+      s.ext[0] >= 16) {
+    int64_t kb[EXSUM_MAX_DIMS];
+    for (int i = 0; i < d; ++i) kb[i] = s.k[i];
+    return bdbs_host_pipelined(s, kb, h_in, h_out, dtype, op);
+  }
   size_t ws_bytes = 0;
   rc = exsum_route_workspace_bytes(route, dtype, op, modulus, d, ext, box, &ws_bytes);
   if (rc) return rc;

@@ -262,3 +262,26 @@ def test_high_dimensional_routes(ex, d):
                 assert ok, (d, route, ratio)
             else:
                 assert _bits_equal(got, want), (d, mono, route, shape, box)
+
+
+@pytest.mark.parametrize("shape,box,dt", [
+    ((520, 130, 256), (16, 4, 8), np.float32),      # 69 MB, uneven chunks
+    ((300, 256, 128), (8, 8, 8), np.float64),       # 78 MB
+    ((1000, 8192), (33, 5), np.int64),              # 65 MB, d = 2, k0 not a power of 2
+    ((257, 256, 256), (1, 4, 4), np.float32),       # k0 = 1: no axis-0 stage
+    ((129, 256, 512), (100, 3, 2), np.int64),       # max, window close to the extent
+])
+def test_host_bdbs_pipelined_is_exact(ex, shape, box, dt):
+    """Numpy-in/numpy-out BDBS >= 64 MB runs pipelined over axis-0 chunks
+    (H2D / compute / D2H overlapped); bit-identical to the oracle."""
+    rng = np.random.default_rng(sum(shape))
+    if np.dtype(dt).kind == "f":
+        a = rng.standard_normal(shape).astype(dt)
+        mono = "add-f32" if dt == np.float32 else "add-f64"
+        op = "add"
+    else:
+        a = rng.integers(-2**40, 2**40, size=shape, dtype=np.int64)
+        mono, op = ("max-i64", "max") if box[0] == 100 else ("add-i64", "add")
+    got = _run(ex, "bdbs", mono, a, box, device=False)
+    want = orc.bdbs_included(a, box, op)
+    assert _bits_equal(got, want), (shape, box, mono)
