@@ -81,3 +81,59 @@ def test_random_sweep(ex):
                 ok, ratio, rel = compare(route, got, float64_oracle(route, a, k, orc), a, k, orc)
                 assert ok, (route, mono, shape, box, device, ratio)
         done += 1
+
+
+def _medium_case(rng):
+    d = int(rng.integers(2, 5))
+    w = int(rng.choice([256, 512, 1024, 384, 1000, 4096, 7]))
+    target = int(rng.integers(1_000_000, 8_000_000))
+    rest = max(1, target // w)
+    if d == 2:
+        shape = (rest, w)
+    elif d == 3:
+        a = int(rng.integers(1, max(2, int(rest ** 0.5)) + 1))
+        shape = (a, max(1, rest // a), w)
+    else:
+        a = int(rng.integers(1, max(2, int(rest ** (1 / 3))) + 1))
+        b = int(rng.integers(1, max(2, int(rest ** (1 / 3))) + 1))
+        shape = (a, b, max(1, rest // (a * b)), w)
+    box = tuple(int(rng.choice([1, 2, 3, 4, 8, 16, 32, 64, n, n + 5])) for n in shape)
+    return shape, box
+
+
+def test_random_medium_sweep(ex):
+    """Sizes that reach the large-array kernels (fused pair, axis stream, TMA
+    bulk, SAT chain query, segmented scans); bit-exact monoids + f64 BDBS."""
+    import torch
+
+    n_cases = int(os.environ.get("EXSUM_FUZZ_MEDIUM", "24"))
+    rng = np.random.default_rng(int(os.environ.get("EXSUM_FUZZ_SEED", "2106")) + 1)
+    fns = {"bdbs": ex.bdbs_included, "bdbsc": ex.bdbs_excluded,
+           "box-complement": ex.box_complement_excluded, "sat": ex.sat_included,
+           "satc": ex.sat_excluded, "corners": ex.corners_excluded}
+    done = 0
+    while done < n_cases:
+        shape, box = _medium_case(rng)
+        mono = ["add-i64", "max-i64", "mod-add:1000003", "add-f64"][int(rng.integers(4))]
+        route = ROUTES[int(rng.integers(len(ROUTES)))]
+        if mono == "max-i64" and route in ("bdbsc", "sat", "satc"):
+            continue
+        if mono == "add-f64" and route not in ("bdbs", "corners"):
+            continue
+        if route == "corners" and len(shape) not in (2, 3):
+            continue
+        ops = ex.resolve_monoid(mono)
+        a = (rng.standard_normal(shape) if mono == "add-f64"
+             else rng.integers(-10**9, 10**9, size=shape, dtype=np.int64))
+        got = fns[route](ex.Tensor(ops, torch.from_numpy(a).cuda()), box).data.cpu().numpy()
+        want = orc.ROUTES[route](a, box, mono_op(mono))
+        if route == "corners" and mono == "add-f64" and not np.array_equal(got, want):
+            # a segmented float scan (few long lines) reassociates: the
+            # box-complement tolerance holds (DESIGN §4)
+            k = tuple(min(b, e) for b, e in zip(box, shape))
+            ok, ratio, _ = compare("box-complement", got,
+                                   float64_oracle("box-complement", a, k, orc), a, k, orc)
+            assert ok, (route, mono, shape, box, ratio)
+        else:
+            assert np.array_equal(got.view(np.uint8), want.view(np.uint8)), (route, mono, shape, box)
+        done += 1
