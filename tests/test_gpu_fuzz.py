@@ -101,9 +101,22 @@ def _medium_case(rng):
     return shape, box
 
 
+def _check(route, mono, got, a, box, shape, tag):
+    want = orc.ROUTES[route](a, box, mono_op(mono))
+    if a.dtype.kind != "f" or route == "bdbs" or np.array_equal(got, want):
+        assert np.array_equal(got.view(np.uint8), want.view(np.uint8)), (route, mono, shape, box, tag)
+        return
+    # floats off the bit-exact contract: the route's tolerance (corners: a
+    # segmented scan reassociates; same quantity as box-complement)
+    k = tuple(min(b, e) for b, e in zip(box, shape))
+    r = "box-complement" if route == "corners" else route
+    ok, ratio, _ = compare(r, got, float64_oracle(r, a, k, orc), a, k, orc)
+    assert ok, (route, mono, shape, box, tag, ratio)
+
+
 def test_random_medium_sweep(ex):
     """Sizes that reach the large-array kernels (fused pair, axis stream, TMA
-    bulk, SAT chain query, segmented scans); bit-exact monoids + f64 BDBS."""
+    bulk, SAT chain query, segmented scans), device and host paths."""
     import torch
 
     n_cases = int(os.environ.get("EXSUM_FUZZ_MEDIUM", "24"))
@@ -114,26 +127,41 @@ def test_random_medium_sweep(ex):
     done = 0
     while done < n_cases:
         shape, box = _medium_case(rng)
-        mono = ["add-i64", "max-i64", "mod-add:1000003", "add-f64"][int(rng.integers(4))]
+        mono = ["add-i64", "max-i64", "mod-add:1000003", "add-f64", "add-f32"][int(rng.integers(5))]
         route = ROUTES[int(rng.integers(len(ROUTES)))]
         if mono == "max-i64" and route in ("bdbsc", "sat", "satc"):
             continue
-        if mono == "add-f64" and route not in ("bdbs", "corners"):
-            continue
         if route == "corners" and len(shape) not in (2, 3):
             continue
+        ops = ex.Float32AddOps() if mono == "add-f32" else ex.resolve_monoid(mono)
+        dt = np.dtype(ops.dtype)
+        a = (rng.standard_normal(shape).astype(dt) if dt.kind == "f"
+             else rng.integers(-10**9, 10**9, size=shape, dtype=np.int64))
+        device = bool(rng.random() < 0.7)
+        data = torch.from_numpy(a).cuda() if device else a.copy()
+        got = fns[route](ex.Tensor(ops, data), box).data
+        got = got.cpu().numpy() if device else np.asarray(got)
+        _check(route, mono, got, a, box, shape, "device" if device else "host")
+        done += 1
+
+
+def test_random_large_host(ex):
+    """Host calls of >= 64 MB (the pipelined single-call BDBS and the chunked
+    host routes) on random shapes and boxes."""
+    n_cases = int(os.environ.get("EXSUM_FUZZ_LARGE", "3"))
+    rng = np.random.default_rng(int(os.environ.get("EXSUM_FUZZ_SEED", "2106")) + 2)
+    for _ in range(n_cases):
+        d = int(rng.integers(2, 4))
+        n_last = int(rng.choice([256, 1000, 1024]))
+        n0 = int(rng.integers(64, 600))
+        rows = int(9_000_000 * rng.uniform(1.0, 1.6)) // n_last  # >= 9e6 elements (>= 64 MB in 8 B)
+        shape = (n0, rows // n0 + 1, n_last) if d == 3 else (rows, n_last)
+        box = tuple(int(rng.choice([1, 2, 5, 16, 33, n])) for n in shape)
+        mono = ["add-i64", "max-i64", "add-f64"][int(rng.integers(3))]
+        route = ["bdbs", "bdbs", "box-complement"][int(rng.integers(3))]
         ops = ex.resolve_monoid(mono)
         a = (rng.standard_normal(shape) if mono == "add-f64"
              else rng.integers(-10**9, 10**9, size=shape, dtype=np.int64))
-        got = fns[route](ex.Tensor(ops, torch.from_numpy(a).cuda()), box).data.cpu().numpy()
-        want = orc.ROUTES[route](a, box, mono_op(mono))
-        if route == "corners" and mono == "add-f64" and not np.array_equal(got, want):
-            # a segmented float scan (few long lines) reassociates: the
-            # box-complement tolerance holds
-            k = tuple(min(b, e) for b, e in zip(box, shape))
-            ok, ratio, _ = compare("box-complement", got,
-                                   float64_oracle("box-complement", a, k, orc), a, k, orc)
-            assert ok, (route, mono, shape, box, ratio)
-        else:
-            assert np.array_equal(got.view(np.uint8), want.view(np.uint8)), (route, mono, shape, box)
-        done += 1
+        fn = ex.bdbs_included if route == "bdbs" else ex.box_complement_excluded
+        got = np.asarray(fn(ex.Tensor(ops, a.copy()), box).data)
+        _check(route, mono, got, a, box, shape, "host-large")
