@@ -482,8 +482,8 @@ k_sat_query_rows(const T* __restrict__ S, T* __restrict__ out, QShape q, int64_t
 // row-at-a-time form.  A 4-slot cp.async ring keeps two steps of prefetch in
 // flight (Little's law: ~64 KB per SM at HBM latency).  A work item (chain) is (the other leading coordinates, r); chains
 // are ordered so that CTAs running together share S planes in L2.
-template <class T, int DH, int NT>
-__global__ void __launch_bounds__(256)
+template <class T, int DH, int NT, int kChainThreads>
+__global__ void __launch_bounds__(kChainThreads)
 k_sat_query_chain(const T* __restrict__ S, T* __restrict__ out, QShape q, int64_t chains,
                   const typename AccOf<T>::type* __restrict__ total, int mode, FastMod fm) {
   constexpr int NQ = 1 << (DH - 1);  // patterns of the other leading axes
@@ -506,7 +506,7 @@ k_sat_query_chain(const T* __restrict__ S, T* __restrict__ out, QShape q, int64_
   if constexpr (std::is_same<T, i64>::value) {
     if (mode == QUERY_MOD_COMPLEMENT) tmod = floor_mod((i64)(*total), fm);
   }
-  for (int i = tid; i < 4 * NQ * VE; i += 256) buf[(i / VE) * pitch + (i % VE)] = T(0);
+  for (int i = tid; i < 4 * NQ * VE; i += kChainThreads) buf[(i / VE) * pitch + (i % VE)] = T(0);
   __syncthreads();
 
   for (int64_t ch = blockIdx.x; ch < chains; ch += gridDim.x) {
@@ -562,9 +562,9 @@ k_sat_query_chain(const T* __restrict__ S, T* __restrict__ out, QShape q, int64_
         T* row = b + qq * pitch;
         if (((qvalid >> qq) & 1) && cr >= 0) {
           const T* g = S + qoff[qq] + cr * strc;
-          for (int c = tid * VE; c < n; c += 256 * VE) cp_async16(row + c, g + c);
+          for (int c = tid * VE; c < n; c += kChainThreads * VE) cp_async16(row + c, g + c);
         } else {
-          for (int c = tid; c < n; c += 256) row[c] = T(0);
+          for (int c = tid; c < n; c += kChainThreads) row[c] = T(0);
         }
       }
       cp_async_commit();
@@ -593,7 +593,10 @@ k_sat_query_chain(const T* __restrict__ S, T* __restrict__ out, QShape q, int64_
       const T* hib = buf + (size_t)hi_slot * slot_elems;
       T* dst = out + obase_lead + xc * strc;
       const int xmain = n - kl + 1;  // x < xmain: the high corner x + kl - 1 is in the row
-      for (int x = tid; x < n; x += 256) {
+      // compile-time row length: fully unrolled, so every x's shared and
+      // global addresses are immediate offsets of this step's bases
+#pragma unroll (NT > 0 ? (NT + kChainThreads - 1) / kChainThreads : 1)
+      for (int x = tid; x < n; x += kChainThreads) {
         const int hi = VE + (x < xmain ? x + kl - 1 : n - 1);
         const int lo = VE - 1 + x;  // x - 1; the zero pad for x = 0
         // four base addresses; every pattern's row is a constant offset from one
@@ -730,14 +733,29 @@ int go_query(const T* S, T* out, const QShape& q, int64_t N, const void* total, 
     const size_t smem = (size_t)4 * NQ * (n + VE) * sizeof(T);
     if (smem <= 96 * 1024) {
       const int64_t chains = N / n / q.ext[q.d - 2] * q.k[q.d - 2];
-      const int per_sm = smem <= 50 * 1024 ? 4 : smem <= 64 * 1024 ? 3 : 2;
+      // many chains: 128-thread CTAs (8 outputs of a 1024-wide row per thread
+      // per step amortise the step's staging and ring bookkeeping), at most 4
+      // per SM (more concurrent chains spread the shared S planes past L2:
+      // C4 f32 query 2.24 -> 1.69 ms, C5 f64 0.48 -> 0.435 ms); few chains:
+      // 256 threads each
+      const int tpb = chains >= 2 * (int64_t)num_sms() ? 128 : 256;
+      int per_sm = (int)((200 * 1024) / smem);
+      per_sm = per_sm < 1 ? 1 : per_sm > 4 ? 4 : per_sm;
       const int64_t cap = (int64_t)num_sms() * per_sm;
-      const unsigned gr = (unsigned)(chains < cap ? chains : cap);
+      // equal chain counts per CTA: the fewest CTAs that keep the same rounds
+      const int64_t rounds = (chains + cap - 1) / cap;
+      const unsigned gr = (unsigned)((chains + rounds - 1) / rounds);
 #define EXSUM_CHAIN_N(DH, NT)                                                                  \
   {                                                                                            \
-    auto kfn = k_sat_query_chain<T, DH, NT>;                                                   \
-    ensure_smem((const void*)kfn, smem);                                                       \
-    kfn<<<gr, 256, smem, s>>>(S, out, q, chains, tot, mode, fm);                               \
+    if (tpb == 128) {                                                                          \
+      auto kfn = k_sat_query_chain<T, DH, NT, 128>;                                            \
+      ensure_smem((const void*)kfn, smem);                                                     \
+      kfn<<<gr, 128, smem, s>>>(S, out, q, chains, tot, mode, fm);                             \
+    } else {                                                                                   \
+      auto kfn = k_sat_query_chain<T, DH, NT, 256>;                                            \
+      ensure_smem((const void*)kfn, smem);                                                     \
+      kfn<<<gr, 256, smem, s>>>(S, out, q, chains, tot, mode, fm);                             \
+    }                                                                                          \
   }
 #define EXSUM_CHAIN(DH)                                                                        \
   {                                                                                            \
