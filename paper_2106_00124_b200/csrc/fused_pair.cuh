@@ -52,6 +52,23 @@ __host__ __device__ constexpr int fp_unit_rows(int C, int K1) {
                                                 : (16 / K1 > 0 ? 16 / K1 : 1) * K1;
 }
 
+// Stage layout: a row of 16-byte vectors with vector v stored at
+// v ^ ((v >> 3) & (CV - 1)) (CV = vectors per lane chunk).  Within every
+// aligned group of 8 vectors this is a permutation, so the streaming phase
+// (thread t <-> vector t) stays conflict-free, and the row op's stride-CV
+// accesses (lane L <-> vector CV*L + c, any shift c) hit 8 distinct 16-byte
+// bank groups per quarter warp -- padding the chunks (the previous layout)
+// left a 2-way conflict on the streaming side whenever CV < 8.
+template <int CV>
+__device__ __forceinline__ int fp_swz(int v) {
+  return v ^ ((v >> 3) & (CV - 1));
+}
+__host__ __device__ constexpr bool fp_swizzled(int CV, int MODE) { return CV < 8 && MODE != ROW_EXCL; }
+// chunk stride in 16-byte vectors: CV when swizzled, else padded to odd
+__host__ __device__ constexpr int fp_chunk_stride(int CV, int MODE) {
+  return fp_swizzled(CV, MODE) ? CV : ((CV + 1) | 1);
+}
+
 template <class T, class Op, int C, int K1, int MODE, int TV>
 // narrow rows ask for more resident CTAs: a register cap that raises the warps
 // per SM there (4-byte, 64-thread CTAs: 12, C3b 0.033 -> 0.030 ms; 8-byte,
@@ -66,9 +83,19 @@ k_fused_pair(const T* __restrict__ in, T* __restrict__ out, int64_t outer, int64
   constexpr int NT = N2 / TV;          // threads: one TV-element column vector each
   constexpr int NW = NT / 32;
   constexpr int CV = C / VE;           // vectors per lane chunk
-  constexpr int PSV = (CV + 1) | 1;    // padded chunk stride in vectors (odd)
-  constexpr int CH = PSV * VE;         // padded chunk stride (elements)
-  constexpr int ROWP = 32 * CH;        // padded row length (elements)
+  // stage layout (fp_stage): XOR-swizzled rows where chunks are narrower
+  // than 8 vectors (the padded layout conflicts 2-way there on the streaming
+  // side) except under the prefix/suffix row op, whose many chunk accesses
+  // would each pay the lane-dependent swizzle in address arithmetic (C2 max
+  // 0.084 -> 0.090 ms); padded chunks (odd stride) otherwise
+  constexpr bool SWZ = fp_swizzled(CV, MODE);
+  constexpr int CH = fp_chunk_stride(CV, MODE) * VE;  // chunk stride (elements)
+  constexpr int ROWP = 32 * CH;                       // stage row length (elements)
+  // stage offset of element e of a row / of vector v of lane L's chunk
+  auto eoff = [](int64_t e) -> int64_t {
+    if constexpr (SWZ) return fp_swz<CV>((int)(e / VE)) * VE + (e % VE);
+    else return (e / C) * CH + (e % C);
+  };
   constexpr int K2 = K1;
   constexpr int M2 = C / K2;           // row-op blocks per lane chunk
   constexpr int G = fp_unit_rows(C, K1) / K1;  // blocks per unit
@@ -83,7 +110,8 @@ k_fused_pair(const T* __restrict__ in, T* __restrict__ out, int64_t outer, int64
   const int lane = tid & 31;
   const int warp = tid >> 5;
   const int col = tid * TV;
-  const int pcol = (col / C) * CH + (col % C);
+  static_assert(TV == VE, "the stage swizzle assumes 16-byte column vectors");
+  const int pcol = SWZ ? fp_swz<CV>(tid) * VE : (col / C) * CH + (col % C);  // this thread's column vector in a stage row
   const T ident = Op::template identity<T>();
   const T tot = total ? (T)(*total) : T(0);
   const bool epi = total != nullptr;
@@ -213,11 +241,16 @@ k_fused_pair(const T* __restrict__ in, T* __restrict__ out, int64_t outer, int64
         const int rr = warp + ri * NW;
         if (rr >= rows_u) break;
         T* wrow = wst + rr * ROWP;
-        T* mine = wrow + lane * CH;
+        T* mine = wrow + lane * CH;  // padded layout: this lane's chunk
+        // vector v of lane L's chunk (L = lane or lane + 1)
+        auto cvec = [&](int L, int v) -> T* {
+          if constexpr (SWZ) return wrow + fp_swz<CV>(L * CV + v) * VE;
+          else return mine + (L - lane) * CH + v * VE;
+        };
         T a[C];
 #pragma unroll
         for (int v = 0; v < CV; ++v) {
-          const VT q = *reinterpret_cast<const VT*>(mine + v * VE);
+          const VT q = *reinterpret_cast<const VT*>(cvec(lane, v));
 #pragma unroll
           for (int j = 0; j < VE; ++j) a[v * VE + j] = q.v[j];
         }
@@ -239,7 +272,7 @@ k_fused_pair(const T* __restrict__ in, T* __restrict__ out, int64_t outer, int64
           if (lane < 31) {
 #pragma unroll
             for (int v = 0; v < NBV; ++v)
-              nbv[v] = *reinterpret_cast<const VT*>(wrow + (lane + 1) * CH + v * VE);
+              nbv[v] = *reinterpret_cast<const VT*>(cvec(lane + 1, v));
           }
 #pragma unroll
           for (int j = 0; j < M2; ++j) {
@@ -290,7 +323,7 @@ k_fused_pair(const T* __restrict__ in, T* __restrict__ out, int64_t outer, int64
                 q.v[j] = epi ? OpAdd::inverse<T>(tot, w) : w;
               }
             }
-            *reinterpret_cast<VT*>(mine + v * VE) = q;
+            *reinterpret_cast<VT*>(cvec(lane, v)) = q;
           }
         } else {
           // full-row prefix / suffix.  The lane chunk is cut into SUB
@@ -347,7 +380,7 @@ k_fused_pair(const T* __restrict__ in, T* __restrict__ out, int64_t outer, int64
                 }
 #pragma unroll
               for (int q = 0; q < SUB; ++q)
-                *reinterpret_cast<VT*>(mine + q * CS + jv * VE) = tq[q];
+                *reinterpret_cast<VT*>(cvec(lane, (q * CS) / VE + jv)) = tq[q];
             }
           }
           __syncwarp();
@@ -366,7 +399,8 @@ k_fused_pair(const T* __restrict__ in, T* __restrict__ out, int64_t outer, int64
               const int64_t y0 = (int64_t)lane * C + v * VE + kx;
               VT sq;
               if (y0 < N2) {
-                sq = *reinterpret_cast<const VT*>(wrow + (y0 / C) * CH + (y0 % C));
+                if constexpr (SWZ) sq = *reinterpret_cast<const VT*>(wrow + eoff(y0));
+                else sq = *reinterpret_cast<const VT*>(wrow + (y0 / C) * CH + (y0 % C));
               } else {
 #pragma unroll
                 for (int j = 0; j < VE; ++j) sq.v[j] = ident;
@@ -385,7 +419,9 @@ k_fused_pair(const T* __restrict__ in, T* __restrict__ out, int64_t outer, int64
             for (int e = 0; e < C; ++e) {
               const int q = e / CS;
               const int64_t y = (int64_t)lane * C + e + kx;
-              const T sv = y < N2 ? wrow[(y / C) * CH + (y % C)] : ident;
+              T sv = ident;
+              if constexpr (SWZ) { if (y < N2) sv = wrow[eoff(y)]; }
+              else { if (y < N2) sv = wrow[(y / C) * CH + (y % C)]; }
               const T ov = Op::apply(Op::apply(pe[q], sv), tail);
               pe[q] = Op::apply(pe[q], a[e]);
               a[e] = ov;
@@ -397,7 +433,7 @@ k_fused_pair(const T* __restrict__ in, T* __restrict__ out, int64_t outer, int64
             VT q;
 #pragma unroll
             for (int j = 0; j < VE; ++j) q.v[j] = a[v * VE + j];
-            *reinterpret_cast<VT*>(mine + v * VE) = q;
+            *reinterpret_cast<VT*>(cvec(lane, v)) = q;
           }
         }
         __syncwarp();
@@ -433,8 +469,7 @@ int go_pair(const T* in, T* out, int64_t outer, int64_t n1, int64_t kx,
   constexpr int N2 = 32 * C;
   constexpr int NT = N2 / TV;
   constexpr int CV = C / VE;
-  constexpr int PSV = (CV + 1) | 1;
-  constexpr int ROWP = 32 * PSV * VE;
+  constexpr int ROWP = 32 * fp_chunk_stride(CV, MODE) * VE;
   constexpr int U = fp_unit_rows(C, K1);
   const size_t smem = ((size_t)2 * U * N2 + (size_t)U * ROWP) * sizeof(T);
   if (smem > 220 * 1024) return -1;
