@@ -1,0 +1,391 @@
+// block_fused.cu -- the windowed passes of the trailing m axes in one pass
+// over HBM, for arrays whose trailing block fits in shared memory.
+//
+// bdbs_included runs windowed_sum_axis (reference pkg/src/exsum/scan.py:61-102)
+// along axes 0..d-1 in order (included.py:124-129).  When the last m axes of a
+// C-order array form a small contiguous block -- the higher-dimensional
+// configurations of the dimension sweep, 28^5, 16^6, 64^4 -- every pass along
+// those axes stays inside one block, so a CTA can stage G whole blocks in
+// shared memory, run the m passes there in axis order, and write the result
+// once: 2 N s bytes for the m passes instead of 2 m N s.
+//
+// B200 mapping:
+//   * stage in / out with coalesced 16-byte global accesses (4 loads in
+//     flight per thread, streaming evict-first); shared memory holds the blocks with the last axis padded
+//     to an odd row length, so the row pass (thread per row) and the strided
+//     passes (thread per column, consecutive threads on consecutive columns)
+//     are both free of bank conflicts;
+//   * one thread walks one line of the axis with the window K known at compile
+//     time: block b's raw values and the next block's raw values rotate through
+//     registers, so each pass reads and writes every shared element once;
+//   * the association is the reference's (in-block right-nested suffix,
+//     left-nested prefix of the next block, one stitch combine; the last block
+//     keeps its suffix), so float results stay bit-identical;
+//   * tiles of G blocks keep ~32 KB of shared memory per CTA: several CTAs per
+//     SM overlap one tile's staging with another's passes.
+// The BDBSC complement epilogue (excluded.py:72-75) rides on the stores.
+#include "exsum_common.cuh"
+#include "exsum_launch.h"
+
+namespace exsum {
+
+// x / d for x < 2^32 / d (tile-local indices): one high multiply; magic 0
+// stands for d == 1 (ceil(2^32 / 1) does not fit 32 bits)
+__device__ __forceinline__ uint32_t bf_div(uint32_t x, uint32_t magic) {
+  return magic ? __umulhi(x, magic) : x;
+}
+
+// In-place windowed pass over one line p[0], p[st], ..., p[(n-1) st]
+// (scan.py:72-102 restated with register rotation).
+template <class T, class Op, int K>
+__device__ __forceinline__ void bf_line(T* p, int n, int st) {
+  T cur[K];
+  const int l0 = n < K ? n : K;
+#pragma unroll
+  for (int r = 0; r < K; ++r)
+    if (r < l0) cur[r] = p[r * st];
+#pragma unroll 2
+  for (int bs = 0; bs < n; bs += K) {
+    const int blen = n - bs < K ? n - bs : K;
+#pragma unroll
+    for (int r = K - 2; r >= 0; --r)
+      if (r < blen - 1) cur[r] = Op::apply(cur[r], cur[r + 1]);
+    T* q = p + bs * st;
+    if (bs + K >= n) {  // last block: out = S
+#pragma unroll
+      for (int r = 0; r < K; ++r)
+        if (r < blen) q[r * st] = cur[r];
+      break;
+    }
+    const int nlen = n - bs - K < K ? n - bs - K : K;
+    T nxt[K];
+#pragma unroll
+    for (int r = 0; r < K; ++r)
+      if (r < nlen) nxt[r] = q[(K + r) * st];
+    q[0] = cur[0];
+    T P = nxt[0];
+#pragma unroll
+    for (int r = 1; r < K; ++r) {
+      const int jj = r - 1;
+      if (jj >= 1 && jj < nlen) P = Op::apply(P, nxt[jj]);
+      q[r * st] = Op::apply(cur[r], P);
+    }
+#pragma unroll
+    for (int r = 0; r < K; ++r) cur[r] = nxt[r];
+  }
+}
+
+// Two lines in lockstep (p0, p1; same length and stride): independent chains
+// interleaved, so one thread keeps twice the shared loads in flight.
+template <class T, class Op, int K>
+__device__ __forceinline__ void bf_line2(T* p0, T* p1, int n, int st) {
+  T c0[K], c1[K];
+  const int l0 = n < K ? n : K;
+#pragma unroll
+  for (int r = 0; r < K; ++r)
+    if (r < l0) {
+      c0[r] = p0[r * st];
+      c1[r] = p1[r * st];
+    }
+  for (int bs = 0; bs < n; bs += K) {
+    const int blen = n - bs < K ? n - bs : K;
+#pragma unroll
+    for (int r = K - 2; r >= 0; --r)
+      if (r < blen - 1) {
+        c0[r] = Op::apply(c0[r], c0[r + 1]);
+        c1[r] = Op::apply(c1[r], c1[r + 1]);
+      }
+    T* q0 = p0 + bs * st;
+    T* q1 = p1 + bs * st;
+    if (bs + K >= n) {
+#pragma unroll
+      for (int r = 0; r < K; ++r)
+        if (r < blen) {
+          q0[r * st] = c0[r];
+          q1[r * st] = c1[r];
+        }
+      break;
+    }
+    const int nlen = n - bs - K < K ? n - bs - K : K;
+    T x0[K], x1[K];
+#pragma unroll
+    for (int r = 0; r < K; ++r)
+      if (r < nlen) {
+        x0[r] = q0[(K + r) * st];
+        x1[r] = q1[(K + r) * st];
+      }
+    q0[0] = c0[0];
+    q1[0] = c1[0];
+    T P0 = x0[0], P1 = x1[0];
+#pragma unroll
+    for (int r = 1; r < K; ++r) {
+      const int jj = r - 1;
+      if (jj >= 1 && jj < nlen) {
+        P0 = Op::apply(P0, x0[jj]);
+        P1 = Op::apply(P1, x1[jj]);
+      }
+      q0[r * st] = Op::apply(c0[r], P0);
+      q1[r * st] = Op::apply(c1[r], P1);
+    }
+#pragma unroll
+    for (int r = 0; r < K; ++r) {
+      c0[r] = x0[r];
+      c1[r] = x1[r];
+    }
+  }
+}
+
+// K: the window of every fused axis with a pass (k > 1); the dimension sweep's
+// boxes are cubic, so one compile-time window covers them
+#define BF_UNR 4
+
+template <class T, class Op, int K, bool VEC>
+__global__ void __launch_bounds__(256, 2)
+k_block_fused(const T* __restrict__ in, T* __restrict__ out, int64_t nblocks, BlockSpec bs,
+              const typename AccOf<T>::type* __restrict__ total) {
+  constexpr int VE = 16 / sizeof(T);
+  extern __shared__ __align__(16) unsigned char smem[];
+  T* sm = reinterpret_cast<T*>(smem);
+  const int tid = threadIdx.x;
+  const int nt = blockDim.x;
+  const int nl = bs.n[bs.m - 1];  // row length (last axis)
+  const int rowp = bs.rowp;
+  const T tot = total ? (T)(*total) : T(0);
+  const bool epi = total != nullptr;
+  const int64_t ntiles = (nblocks + bs.G - 1) / bs.G;
+
+  for (int64_t tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
+    const int64_t b0 = tile * bs.G;
+    const int g = (int)(nblocks - b0 < bs.G ? nblocks - b0 : bs.G);
+    const int E = g * (int)bs.B;  // elements of this tile
+    const T* src = in + b0 * bs.B;
+    T* dst = out + b0 * bs.B;
+    // ---- stage in: element e -> shared (e / nl) * rowp + e % nl.  16-byte
+    // coalesced loads (tile offsets are multiples of 16 bytes when VEC),
+    // BF_UNR of them in flight per thread before the scattered shared stores
+    if constexpr (VEC) {
+      for (int e0 = tid * VE; e0 < E; e0 += nt * VE * BF_UNR) {
+        Vec<T, VE> v[BF_UNR];
+#pragma unroll
+        for (int u = 0; u < BF_UNR; ++u)
+          if (e0 + u * nt * VE < E) v[u] = ld_stream<T, VE>(src + e0 + u * nt * VE);
+#pragma unroll
+        for (int u = 0; u < BF_UNR; ++u) {
+          const int e = e0 + u * nt * VE;
+          if (e < E) {
+            int row = (int)bf_div((uint32_t)e, bs.magic_nl);
+            int col = e - row * nl;
+#pragma unroll
+            for (int j = 0; j < VE; ++j) {
+              sm[row * rowp + col] = v[u].v[j];
+              if (++col == nl) {
+                col = 0;
+                ++row;
+              }
+            }
+          }
+        }
+      }
+    } else {
+      for (int e0 = tid; e0 < E; e0 += nt * BF_UNR) {
+        T v[BF_UNR];
+#pragma unroll
+        for (int u = 0; u < BF_UNR; ++u)
+          if (e0 + u * nt < E) v[u] = ld1(src + e0 + u * nt);
+#pragma unroll
+        for (int u = 0; u < BF_UNR; ++u) {
+          const int e = e0 + u * nt;
+          if (e < E) {
+            const int row = (int)bf_div((uint32_t)e, bs.magic_nl);
+            sm[row * rowp + (e - row * nl)] = v[u];
+          }
+        }
+      }
+    }
+    __syncthreads();
+    // ---- the passes, axes in order (included.py:127)
+    for (int j = 0; j < bs.m; ++j) {
+      if (bs.k[j] > 1) {
+        const int n = bs.n[j];
+        if (j == bs.m - 1) {
+          const int rows = E / nl;
+          int r = tid;
+          if constexpr (sizeof(T) == 4)
+            for (; r + nt < rows; r += 2 * nt) bf_line2<T, Op, K>(sm + r * rowp, sm + (r + nt) * rowp, n, 1);
+          for (; r < rows; r += nt) bf_line<T, Op, K>(sm + r * rowp, n, 1);
+
+        } else {
+          // lines: (outer o, inner i); inner runs over the valid elements of
+          // the later axes, i -> (i / nl) * rowp + i % nl in the padded layout
+          const int inner = bs.inner[j];       // valid elements after axis j
+          const int inner_p = inner / nl * rowp;  // padded stride of axis j
+          const int lines = E / n;              // = outer * inner
+          auto line_at = [&](int L) -> T* {
+            const int o = (int)bf_div((uint32_t)L, bs.magic_inner[j]);
+            const int i = L - o * inner;
+            const int ir = (int)bf_div((uint32_t)i, bs.magic_nl);
+            return sm + (o * n * inner_p + ir * rowp + (i - ir * nl));
+          };
+          int L = tid;
+          if constexpr (sizeof(T) == 4)
+            for (; L + nt < lines; L += 2 * nt) bf_line2<T, Op, K>(line_at(L), line_at(L + nt), n, inner_p);
+          for (; L < lines; L += nt) bf_line<T, Op, K>(line_at(L), n, inner_p);
+        }
+        __syncthreads();
+      }
+    }
+    // ---- stage out (+ BDBSC complement)
+    if constexpr (VEC) {
+      for (int e = tid * VE; e < E; e += nt * VE) {
+        Vec<T, VE> v;
+        int row = (int)bf_div((uint32_t)e, bs.magic_nl);
+        int col = e - row * nl;
+#pragma unroll
+        for (int j = 0; j < VE; ++j) {
+          const T w = sm[row * rowp + col];
+          v.v[j] = epi ? OpAdd::inverse<T>(tot, w) : w;
+          if (++col == nl) {
+            col = 0;
+            ++row;
+          }
+        }
+        st_stream<T, VE>(dst + e, v);
+      }
+    } else {
+      for (int e = tid; e < E; e += nt) {
+        const int row = (int)bf_div((uint32_t)e, bs.magic_nl);
+        const T w = sm[row * rowp + (e - row * nl)];
+        st1(dst + e, epi ? OpAdd::inverse<T>(tot, w) : w);
+      }
+    }
+    __syncthreads();  // the next tile overwrites the stage
+  }
+}
+
+static uint32_t bf_magic(uint32_t d) {
+  // ceil(2^32 / d): exact quotients for x < 2^32 / d; 0 marks d == 1
+  return d <= 1 ? 0u : (uint32_t)((((uint64_t)1 << 32) + d - 1) / d);
+}
+
+static int64_t bf_env(const char* name, int64_t dflt) {
+  const char* e = getenv(name);
+  return (e && *e) ? atoll(e) : dflt;
+}
+
+int block_fused_plan(int dtype, int d, const int64_t* ext, const int64_t* k, int first_axis,
+                     BlockSpec* out) {
+  if (bf_env("EXSUM_BLOCK_FUSE", 1) == 0) return 0;
+  const int64_t es = (int64_t)dtype_size(dtype);
+  // 4-byte elements only: with 8-byte lines the in-shared line walks are
+  // latency-bound below the unfused passes (C3 int64 max: 64^4 0.244 vs 0.216 ms,
+  // 28^5 0.301 vs 0.290 ms)
+  if (es != 4 && bf_env("EXSUM_BLOCK_FUSE", 1) < 2) return 0;
+  const int64_t budget = bf_env("EXSUM_BF_KB", 96) * 1024;
+  const int64_t tile_target = bf_env("EXSUM_BF_TILE_KB", 32) * 1024;
+  const int64_t nl = ext[d - 1];
+  const int64_t rowp = nl | 1;  // odd padded row length
+  // the largest m (>= 2 axes, not before first_axis) whose padded block fits,
+  // with at least two passes inside and every window a supported size
+  for (int m = d - first_axis < BF_MAX ? d - first_axis : BF_MAX; m >= 2; --m) {
+    int64_t B = 1;
+    for (int a = d - m; a < d; ++a) B *= ext[a];
+    const int64_t bytes = B / nl * rowp * es;
+    if (bytes > budget) continue;
+    int passes = 0;
+    bool ok = true;
+    int64_t kw = 0;
+    for (int a = d - m; a < d; ++a) {
+      if (k[a] > 1) {
+        ++passes;
+        if (kw == 0) kw = k[a];
+        if (k[a] != kw || !(kw == 2 || kw == 4 || (kw == 8 && es == 4))) ok = false;
+      }
+    }
+    if (!ok || passes < 2) return 0;  // a smaller m has no more passes than this one
+    BlockSpec bs;
+    bs.m = m;
+    bs.B = B;
+    bs.rowp = (int)rowp;
+    int64_t G = tile_target / bytes;
+    if (G < 1) G = 1;
+    if (G * B > (1 << 20)) G = ((int64_t)1 << 20) / B;  // tile-local indices stay small
+    if (G < 1) return 0;
+    bs.G = (int)G;
+    int64_t inner = B;
+    for (int j = 0; j < m; ++j) {
+      bs.n[j] = (int)ext[d - m + j];
+      bs.k[j] = (int)k[d - m + j];
+      inner /= ext[d - m + j];
+      bs.inner[j] = (int)inner;
+      bs.magic_inner[j] = bf_magic((uint32_t)(inner > 0 ? inner : 1));
+    }
+    bs.magic_nl = bf_magic((uint32_t)nl);
+    bs.K = (int)kw;
+    // threads: one per line of the pass with the fewest lines (every pass
+    // walks its lines sequentially, so idle threads only add CTA size)
+    int64_t nmax = 1;
+    for (int a = d - m; a < d; ++a)
+      if (k[a] > 1 && ext[a] > nmax) nmax = ext[a];
+    int64_t nt = (G * B / nmax + 31) / 32 * 32;
+    bs.threads = (int)(nt < 64 ? 64 : (nt > 256 ? 256 : nt));
+    bs.smem = (size_t)G * (size_t)bytes;
+    *out = bs;
+    return 1;
+  }
+  return 0;
+}
+
+template <class T, class Op, int K>
+static int go_block(const T* in, T* out, int64_t N, const BlockSpec& bs,
+                    const typename AccOf<T>::type* total, cudaStream_t s) {
+  const int64_t nblocks = N / bs.B;
+  int per_sm = (int)((228 * 1024) / (bs.smem + 1024));
+  if (per_sm > 2048 / bs.threads) per_sm = 2048 / bs.threads;
+  if (per_sm > 32) per_sm = 32;
+  if (per_sm < 1) per_sm = 1;
+  const int64_t ntiles = (nblocks + bs.G - 1) / bs.G;
+  int64_t grid = (int64_t)num_sms() * per_sm;
+  if (grid > ntiles) grid = ntiles;
+  const bool vec = ((uintptr_t)in % 16 == 0) && ((uintptr_t)out % 16 == 0) &&
+                   ((bs.B * (int64_t)sizeof(T)) % 16 == 0);
+  if (vec) {
+    ensure_smem((const void*)k_block_fused<T, Op, K, true>, bs.smem);
+    k_block_fused<T, Op, K, true><<<(unsigned)grid, bs.threads, bs.smem, s>>>(in, out, nblocks, bs,
+                                                                             total);
+  } else {
+    ensure_smem((const void*)k_block_fused<T, Op, K, false>, bs.smem);
+    k_block_fused<T, Op, K, false><<<(unsigned)grid, bs.threads, bs.smem, s>>>(in, out, nblocks, bs,
+                                                                              total);
+  }
+  return 1;
+}
+
+template <class T, class Op>
+static int go_block_k(const T* in, T* out, int64_t N, const BlockSpec& bs,
+                      const typename AccOf<T>::type* total, cudaStream_t s) {
+  switch (bs.K) {
+    case 2: return go_block<T, Op, 2>(in, out, N, bs, total, s);
+    case 4: return go_block<T, Op, 4>(in, out, N, bs, total, s);
+    // windows of 16 (and 8 for 8-byte lines) spill at two CTAs per SM; the
+    // plan rejects them
+    case 8:
+      if constexpr (sizeof(T) == 4) return go_block<T, Op, 8>(in, out, N, bs, total, s);
+      return -1;
+  }
+  return -1;
+}
+
+int launch_block_fused(int dtype, int op, const void* in, void* out, int64_t N, const BlockSpec& bs,
+                       const void* total, cudaStream_t s) {
+  if (dtype == F32 && op == ADD)
+    return go_block_k<float, OpAdd>((const float*)in, (float*)out, N, bs, (const double*)total, s);
+  if (dtype == F64 && op == ADD)
+    return go_block_k<double, OpAdd>((const double*)in, (double*)out, N, bs, (const double*)total, s);
+  if (dtype == I64 && op == ADD)
+    return go_block_k<i64, OpAdd>((const i64*)in, (i64*)out, N, bs, (const i64*)total, s);
+  if (dtype == I64 && op == MAX)
+    return go_block_k<i64, OpMax>((const i64*)in, (i64*)out, N, bs, nullptr, s);
+  return -2;
+}
+
+}  // namespace exsum

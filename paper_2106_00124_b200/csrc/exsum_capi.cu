@@ -251,12 +251,21 @@ int route_bdbs(const Shape& s, int dtype, int op, const void* in, void* out, Are
                      aligned16(out) && (p.count > 2 || aligned16(in));
   PassPlan head = p;
   if (fused) head.count -= 2;
+  // otherwise the trailing axes as one shared-memory block when it fits
+  // (block_fused.cu): the passes along axes >= d - m in one HBM round trip
+  BlockSpec bsp;
+  const bool blockf = !fused && p.count >= 2 && block_fused_plan(dtype, d, s.ext, s.k, 0, &bsp);
+  if (blockf) {
+    head.count = 0;
+    while (head.count < p.count && p.axes[head.count] < d - bsp.m) ++head.count;
+  }
   // BDBSC total: folded into the first pass when a later pass applies it
   PassExtra ex0;
   ex0.kind = 2;
   ex0.buf = partials;
   ex0.cap = reduce_partials_count();
-  const bool piggy = complement && !given_total && head.count >= 1 && (fused || head.count >= 2);
+  const bool piggy =
+      complement && !given_total && head.count >= 1 && (fused || blockf || head.count >= 2);
   if (complement && !piggy) full_total();
   auto finish_total = [&]() -> int {
     if (piggy && live) {
@@ -270,12 +279,19 @@ int route_bdbs(const Shape& s, int dtype, int op, const void* in, void* out, Are
   };
   const void* mid = in;
   if (head.count > 0) {
-    void* head_dst = fused ? other : out;
-    void* head_other = fused ? out : other;
-    int rc = run_chain(s, head, dtype, op, in, head_dst, head_other, fused ? nullptr : total, st,
-                       launches, live, piggy ? &ex0 : nullptr, finish_total);
+    const bool tail_kernel = fused || blockf;
+    void* head_dst = tail_kernel ? other : out;
+    void* head_other = tail_kernel ? out : other;
+    int rc = run_chain(s, head, dtype, op, in, head_dst, head_other, tail_kernel ? nullptr : total,
+                       st, launches, live, piggy ? &ex0 : nullptr, finish_total);
     if (rc) return rc;
     mid = head_dst;
+  }
+  if (blockf && live) {
+    ProfScope ps("block_fused", 2.0 * (double)s.N * es, st);
+    int rc = launch_block_fused(dtype, op, mid, out, s.N, bsp, total, st);
+    if (rc < 0) return fail(EXSUM_ECONFIG, "no block kernel for this dtype/operator");
+    *launches += rc;
   }
   if (fused && live) {
     ProfScope ps("fused_pair", 2.0 * (double)s.N * es, st);

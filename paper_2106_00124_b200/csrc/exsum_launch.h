@@ -82,6 +82,28 @@ int launch_fused_pair(int dtype, int op, const void* in, void* out, int64_t oute
                       int64_t n2, int64_t k1, int64_t k2, int mode, const void* total,
                       const void* Tail, cudaStream_t s);
 
+// Trailing-block fusion (block_fused.cu): the windowed passes along the last m
+// axes in one kernel when a block of those axes (last axis padded to an odd
+// length) fits in shared memory.  block_fused_plan picks the largest such m
+// (axes >= first_axis, at least two passes, windows 2/4/8/16) and returns 1.
+#define BF_MAX 6
+struct BlockSpec {
+  int m = 0;
+  int n[BF_MAX], k[BF_MAX], inner[BF_MAX];
+  uint32_t magic_inner[BF_MAX];
+  uint32_t magic_nl = 0;
+  int64_t B = 0;    // elements per block
+  int rowp = 0;     // padded row length
+  int G = 1;        // blocks per CTA tile
+  int K = 0;        // the window of every fused axis with a pass
+  int threads = 256;
+  size_t smem = 0;  // bytes per tile
+};
+int block_fused_plan(int dtype, int d, const int64_t* ext, const int64_t* k, int first_axis,
+                     BlockSpec* out);
+int launch_block_fused(int dtype, int op, const void* in, void* out, int64_t N, const BlockSpec& bs,
+                       const void* total, cudaStream_t s);
+
 // ---------------------------------------------- sat / satc / mod-add (sat.cu)
 
 // Inclusive running fold (ops.accumulate: np.add / np.maximum .accumulate)

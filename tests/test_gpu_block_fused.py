@@ -1,0 +1,123 @@
+"""GPU parity for the trailing-block fusion (csrc/block_fused.cu): the
+windowed passes of the last m axes of bdbs_included (included.py:124-129,
+scan.py:61-102) run in shared memory in one kernel when a block of those axes
+fits.  The fused kernel keeps the reference's association, so float bdbs stays
+bit-identical to the oracle and to the unfused passes (EXSUM_BLOCK_FUSE=0);
+bdbsc carries the complement epilogue on the fused kernel's stores.
+
+float32 takes the fused kernel by default; EXSUM_BLOCK_FUSE=2 also routes
+8-byte types through it (off by default: slower than the unfused passes
+there), which these tests use to keep that path correct.
+"""
+
+import os
+
+import numpy as np
+import pytest
+
+from oracle import oracle as orc
+from parity import compare, float64_oracle
+
+pytestmark = pytest.mark.gpu
+
+
+@pytest.fixture(scope="module")
+def ex():
+    import torch
+
+    assert torch.cuda.is_available()
+    import paper_2106_00124_b200 as ex
+
+    ex._native.load()
+    return ex
+
+
+def _mono(ex, name):
+    return ex.Float32AddOps() if name == "add-f32" else ex.resolve_monoid(name)
+
+
+def _run(ex, route, mono, arr, box, fuse):
+    import torch
+
+    fn = {"bdbs": ex.bdbs_included, "bdbsc": ex.bdbs_excluded}[route]
+    old = os.environ.get("EXSUM_BLOCK_FUSE")
+    os.environ["EXSUM_BLOCK_FUSE"] = str(fuse)
+    try:
+        data = torch.from_numpy(np.ascontiguousarray(arr)).cuda()
+        out = fn(ex.Tensor(_mono(ex, mono), data), box).data.cpu().numpy()
+        launches = ex._native.last_launch_count()
+    finally:
+        if old is None:
+            del os.environ["EXSUM_BLOCK_FUSE"]
+        else:
+            os.environ["EXSUM_BLOCK_FUSE"] = old
+    return out, launches
+
+
+def _bits_equal(a, b):
+    return a.dtype == b.dtype and np.array_equal(a.view(np.uint8), b.view(np.uint8))
+
+
+def _data(rng, mono, shape):
+    if mono == "add-f32":
+        return rng.standard_normal(shape).astype(np.float32)
+    if mono == "add-f64":
+        return rng.standard_normal(shape)
+    return rng.integers(-2**40, 2**40, size=shape, dtype=np.int64)
+
+
+CASES = [
+    # (shape, box): the C3 shapes scaled down, tails (n % k != 0), k = 1 axes,
+    # k >= n (clamped), extents of 1, several blocks per CTA tile, odd rows
+    ((6, 28, 28, 28), (4, 4, 4, 4)),
+    ((3, 16, 16, 16, 16), (4, 4, 4, 4, 4)),
+    ((5, 64, 64), (4, 4, 4)),
+    ((7, 13, 11), (4, 1, 4)),
+    ((9, 10, 17), (2, 2, 2)),
+    ((4, 3, 5, 7), (4, 4, 4, 4)),
+    ((2, 9, 1, 6), (8, 8, 1, 8)),
+    ((33, 30, 30), (8, 8, 8)),
+    ((1, 12, 12), (4, 4, 4)),
+    ((100, 5), (4, 4)),
+]
+
+
+@pytest.mark.parametrize("shape,box", CASES)
+@pytest.mark.parametrize("mono", ["add-f32", "add-i64", "max-i64", "add-f64"])
+def test_block_fused_bdbs_exact(ex, shape, box, mono):
+    rng = np.random.default_rng(sum(shape) + len(mono))
+    a = _data(rng, mono, shape)
+    op = "max" if mono == "max-i64" else "add"
+    got, n_fused = _run(ex, "bdbs", mono, a, box, fuse=2)
+    ref, n_plain = _run(ex, "bdbs", mono, a, box, fuse=0)
+    want = orc.ROUTES["bdbs"](a, box, op)
+    assert _bits_equal(got, want), (shape, box, mono)
+    assert _bits_equal(ref, want), (shape, box, mono)
+    assert n_fused <= n_plain
+
+
+@pytest.mark.parametrize("shape,box", CASES[:6])
+@pytest.mark.parametrize("mono", ["add-f32", "add-i64", "add-f64"])
+def test_block_fused_bdbsc(ex, shape, box, mono):
+    rng = np.random.default_rng(7 * sum(shape) + len(mono))
+    a = _data(rng, mono, shape)
+    got, _ = _run(ex, "bdbsc", mono, a, box, fuse=2)
+    if a.dtype.kind == "i":
+        assert _bits_equal(got, orc.ROUTES["bdbsc"](a, box, "add")), (shape, box, mono)
+    else:
+        k = tuple(min(b, e) for b, e in zip(box, shape))
+        ok, ratio, rel = compare("bdbsc", got, float64_oracle("bdbsc", a, k, orc), a, k, orc)
+        assert ok, (shape, box, mono, ratio)
+
+
+def test_block_fused_is_taken_for_c3_shapes(ex):
+    """The C3 float32 shapes of higher dimension run the fused kernel by default
+    (fewer launches than the unfused passes) with identical bits."""
+    rng = np.random.default_rng(3)
+    for shape in [(28,) * 5, (16,) * 6, (64,) * 4]:
+        a = rng.standard_normal(shape).astype(np.float32)
+        box = (4,) * len(shape)
+        got, n_fused = _run(ex, "bdbs", "add-f32", a, box, fuse=1)
+        ref, n_plain = _run(ex, "bdbs", "add-f32", a, box, fuse=0)
+        assert _bits_equal(got, ref), shape
+        assert n_fused < n_plain, (shape, n_fused, n_plain)
