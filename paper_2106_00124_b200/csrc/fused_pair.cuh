@@ -18,8 +18,9 @@
 //     loads (128 KB at the C4 shape) are in flight while block b is processed;
 //   * the axis-(d-2) pass runs in registers exactly as in pass_strided.cu
 //     (suffix of block b, running prefix of block b+1), writing the k1 output
-//     rows to a padded shared stage (chunk stride an odd number of 16-byte
-//     vectors: conflict-free for both access patterns);
+//     rows to a shared stage laid out conflict-free for both access patterns
+//     (chunk stride an odd number of 16-byte vectors, or an XOR swizzle of
+//     the vectors where chunks are narrower than 8 vectors -- fp_swz);
 //   * after one __syncthreads each warp takes whole rows, each lane a chunk of
 //     C = n2/32 consecutive elements in registers, and runs the row op
 //     (sequential exact in-block scans for ROW_WIN; lane fold + warp scans for
