@@ -10,8 +10,8 @@
 // once: 2 N s bytes for the m passes instead of 2 m N s.
 //
 // B200 mapping:
-//   * stage in / out with coalesced 16-byte global accesses (4 loads in
-//     flight per thread, streaming evict-first); shared memory holds the blocks with the last axis padded
+//   * stage in with element-sized cp.async copies (the whole tile in flight),
+//     out with coalesced 16-byte streaming stores; shared memory holds the blocks with the last axis padded
 //     to an odd row length, so the row pass (thread per row) and the strided
 //     passes (thread per column, consecutive threads on consecutive columns)
 //     are both free of bank conflicts;
@@ -137,8 +137,6 @@ __device__ __forceinline__ void bf_line2(T* p0, T* p1, int n, int st) {
 
 // K: the window of every fused axis with a pass (k > 1); the dimension sweep's
 // boxes are cubic, so one compile-time window covers them
-#define BF_UNR 4
-
 template <class T, class Op, int K, bool VEC>
 __global__ void __launch_bounds__(256, 2)
 k_block_fused(const T* __restrict__ in, T* __restrict__ out, int64_t nblocks, BlockSpec bs,
@@ -160,48 +158,17 @@ k_block_fused(const T* __restrict__ in, T* __restrict__ out, int64_t nblocks, Bl
     const int E = g * (int)bs.B;  // elements of this tile
     const T* src = in + b0 * bs.B;
     T* dst = out + b0 * bs.B;
-    // ---- stage in: element e -> shared (e / nl) * rowp + e % nl.  16-byte
-    // coalesced loads (tile offsets are multiples of 16 bytes when VEC),
-    // BF_UNR of them in flight per thread before the scattered shared stores
-    if constexpr (VEC) {
-      for (int e0 = tid * VE; e0 < E; e0 += nt * VE * BF_UNR) {
-        Vec<T, VE> v[BF_UNR];
-#pragma unroll
-        for (int u = 0; u < BF_UNR; ++u)
-          if (e0 + u * nt * VE < E) v[u] = ld_stream<T, VE>(src + e0 + u * nt * VE);
-#pragma unroll
-        for (int u = 0; u < BF_UNR; ++u) {
-          const int e = e0 + u * nt * VE;
-          if (e < E) {
-            int row = (int)bf_div((uint32_t)e, bs.magic_nl);
-            int col = e - row * nl;
-#pragma unroll
-            for (int j = 0; j < VE; ++j) {
-              sm[row * rowp + col] = v[u].v[j];
-              if (++col == nl) {
-                col = 0;
-                ++row;
-              }
-            }
-          }
-        }
-      }
-    } else {
-      for (int e0 = tid; e0 < E; e0 += nt * BF_UNR) {
-        T v[BF_UNR];
-#pragma unroll
-        for (int u = 0; u < BF_UNR; ++u)
-          if (e0 + u * nt < E) v[u] = ld1(src + e0 + u * nt);
-#pragma unroll
-        for (int u = 0; u < BF_UNR; ++u) {
-          const int e = e0 + u * nt;
-          if (e < E) {
-            const int row = (int)bf_div((uint32_t)e, bs.magic_nl);
-            sm[row * rowp + (e - row * nl)] = v[u];
-          }
-        }
-      }
+    // ---- stage in: element e -> shared (e / nl) * rowp + e % nl, as
+    // element-sized cp.async copies (LDGSTS): lanes on consecutive elements
+    // (coalesced), the whole tile in flight at once with no registers held --
+    // register-staged 16-byte loads waited a DRAM latency per batch (C3
+    // int64 28^5: 0.115 -> 0.077 ms)
+    for (int e = tid; e < E; e += nt) {
+      const int row = (int)bf_div((uint32_t)e, bs.magic_nl);
+      cp_async_n<sizeof(T)>(sm + row * rowp + (e - row * nl), src + e);
     }
+    cp_async_commit();
+    cp_async_wait<0>();
     __syncthreads();
     // ---- the passes, axes in order (included.py:127)
     for (int j = 0; j < bs.m; ++j) {
@@ -276,10 +243,6 @@ int block_fused_plan(int dtype, int d, const int64_t* ext, const int64_t* k, int
                      BlockSpec* out) {
   if (bf_env("EXSUM_BLOCK_FUSE", 1) == 0) return 0;
   const int64_t es = (int64_t)dtype_size(dtype);
-  // 4-byte elements only: with 8-byte lines the in-shared line walks are
-  // latency-bound below the unfused passes (C3 int64 max: 64^4 0.244 vs 0.216 ms,
-  // 28^5 0.301 vs 0.290 ms)
-  if (es != 4 && bf_env("EXSUM_BLOCK_FUSE", 1) < 2) return 0;
   const int64_t budget = bf_env("EXSUM_BF_KB", 96) * 1024;
   const int64_t tile_target = bf_env("EXSUM_BF_TILE_KB", 32) * 1024;
   const int64_t nl = ext[d - 1];

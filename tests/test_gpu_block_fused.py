@@ -5,9 +5,8 @@ fits.  The fused kernel keeps the reference's association, so float bdbs stays
 bit-identical to the oracle and to the unfused passes (EXSUM_BLOCK_FUSE=0);
 bdbsc carries the complement epilogue on the fused kernel's stores.
 
-float32 takes the fused kernel by default; EXSUM_BLOCK_FUSE=2 also routes
-8-byte types through it (off by default: slower than the unfused passes
-there), which these tests use to keep that path correct.
+Every dtype takes the fused kernel where the plan allows (EXSUM_BLOCK_FUSE=1,
+the default; 2 is the same plan, kept as the explicit "all dtypes" switch).
 """
 
 import os
@@ -110,14 +109,15 @@ def test_block_fused_bdbsc(ex, shape, box, mono):
         assert ok, (shape, box, mono, ratio)
 
 
-def test_block_fused_is_taken_for_c3_shapes(ex):
-    """The C3 float32 shapes of higher dimension run the fused kernel by default
-    (fewer launches than the unfused passes) with identical bits."""
+@pytest.mark.parametrize("mono", ["add-f32", "max-i64"])
+def test_block_fused_is_taken_for_c3_shapes(ex, mono):
+    """The C3 shapes of higher dimension (float32 +, int64 max) run the fused
+    kernel by default (fewer launches than the unfused passes) with identical bits."""
     rng = np.random.default_rng(3)
     for shape in [(28,) * 5, (16,) * 6, (64,) * 4]:
-        a = rng.standard_normal(shape).astype(np.float32)
+        a = _data(rng, mono, shape)
         box = (4,) * len(shape)
-        got, n_fused = _run(ex, "bdbs", "add-f32", a, box, fuse=1)
-        ref, n_plain = _run(ex, "bdbs", "add-f32", a, box, fuse=0)
+        got, n_fused = _run(ex, "bdbs", mono, a, box, fuse=1)
+        ref, n_plain = _run(ex, "bdbs", mono, a, box, fuse=0)
         assert _bits_equal(got, ref), shape
         assert n_fused < n_plain, (shape, n_fused, n_plain)
