@@ -75,66 +75,6 @@ __device__ __forceinline__ void bf_line(T* p, int n, int st) {
   }
 }
 
-// Two lines in lockstep (p0, p1; same length and stride): independent chains
-// interleaved, so one thread keeps twice the shared loads in flight.
-template <class T, class Op, int K>
-__device__ __forceinline__ void bf_line2(T* p0, T* p1, int n, int st) {
-  T c0[K], c1[K];
-  const int l0 = n < K ? n : K;
-#pragma unroll
-  for (int r = 0; r < K; ++r)
-    if (r < l0) {
-      c0[r] = p0[r * st];
-      c1[r] = p1[r * st];
-    }
-  for (int bs = 0; bs < n; bs += K) {
-    const int blen = n - bs < K ? n - bs : K;
-#pragma unroll
-    for (int r = K - 2; r >= 0; --r)
-      if (r < blen - 1) {
-        c0[r] = Op::apply(c0[r], c0[r + 1]);
-        c1[r] = Op::apply(c1[r], c1[r + 1]);
-      }
-    T* q0 = p0 + bs * st;
-    T* q1 = p1 + bs * st;
-    if (bs + K >= n) {
-#pragma unroll
-      for (int r = 0; r < K; ++r)
-        if (r < blen) {
-          q0[r * st] = c0[r];
-          q1[r * st] = c1[r];
-        }
-      break;
-    }
-    const int nlen = n - bs - K < K ? n - bs - K : K;
-    T x0[K], x1[K];
-#pragma unroll
-    for (int r = 0; r < K; ++r)
-      if (r < nlen) {
-        x0[r] = q0[(K + r) * st];
-        x1[r] = q1[(K + r) * st];
-      }
-    q0[0] = c0[0];
-    q1[0] = c1[0];
-    T P0 = x0[0], P1 = x1[0];
-#pragma unroll
-    for (int r = 1; r < K; ++r) {
-      const int jj = r - 1;
-      if (jj >= 1 && jj < nlen) {
-        P0 = Op::apply(P0, x0[jj]);
-        P1 = Op::apply(P1, x1[jj]);
-      }
-      q0[r * st] = Op::apply(c0[r], P0);
-      q1[r * st] = Op::apply(c1[r], P1);
-    }
-#pragma unroll
-    for (int r = 0; r < K; ++r) {
-      c0[r] = x0[r];
-      c1[r] = x1[r];
-    }
-  }
-}
-
 // K: the window of every fused axis with a pass (k > 1); the dimension sweep's
 // boxes are cubic, so one compile-time window covers them
 template <class T, class Op, int K, bool VEC>
@@ -176,11 +116,7 @@ k_block_fused(const T* __restrict__ in, T* __restrict__ out, int64_t nblocks, Bl
         const int n = bs.n[j];
         if (j == bs.m - 1) {
           const int rows = E / nl;
-          int r = tid;
-          if constexpr (sizeof(T) == 4)
-            for (; r + nt < rows; r += 2 * nt) bf_line2<T, Op, K>(sm + r * rowp, sm + (r + nt) * rowp, n, 1);
-          for (; r < rows; r += nt) bf_line<T, Op, K>(sm + r * rowp, n, 1);
-
+          for (int r = tid; r < rows; r += nt) bf_line<T, Op, K>(sm + r * rowp, n, 1);
         } else {
           // lines: (outer o, inner i); inner runs over the valid elements of
           // the later axes, i -> (i / nl) * rowp + i % nl in the padded layout
@@ -193,10 +129,7 @@ k_block_fused(const T* __restrict__ in, T* __restrict__ out, int64_t nblocks, Bl
             const int ir = (int)bf_div((uint32_t)i, bs.magic_nl);
             return sm + (o * n * inner_p + ir * rowp + (i - ir * nl));
           };
-          int L = tid;
-          if constexpr (sizeof(T) == 4)
-            for (; L + nt < lines; L += 2 * nt) bf_line2<T, Op, K>(line_at(L), line_at(L + nt), n, inner_p);
-          for (; L < lines; L += nt) bf_line<T, Op, K>(line_at(L), n, inner_p);
+          for (int L = tid; L < lines; L += nt) bf_line<T, Op, K>(line_at(L), n, inner_p);
         }
         __syncthreads();
       }
