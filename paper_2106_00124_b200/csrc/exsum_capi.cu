@@ -246,6 +246,16 @@ int route_bdbs(const Shape& s, int dtype, int op, const void* in, void* out, Are
     return EXSUM_OK;
   }
   const int d = s.d;
+  if (!complement && l2pipe_ok(dtype, op, d, s.ext, s.k) && aligned16(in) && aligned16(out)) {
+    void* ws = ar.take(l2pipe_workspace_bytes(s.ext));
+    if (live) {
+      ProfScope ps("l2pipe", 2.0 * (double)s.N * es, st);
+      const int rc = launch_l2pipe(0, in, out, s.ext, nullptr, ws, st);
+      if (rc < 0) return fail(EXSUM_ECUDA, "L2-pipelined kernel failed to launch");
+      *launches += rc;
+    }
+    return EXSUM_OK;
+  }
   const bool fused = p.count >= 2 && p.axes[p.count - 2] == d - 2 && p.axes[p.count - 1] == d - 1 &&
                      fused_pair_ok(dtype, op, s.ext[d - 1], s.k[d - 2], s.k[d - 1], ROW_WIN) &&
                      aligned16(out) && (p.count > 2 || aligned16(in));
@@ -367,6 +377,31 @@ int route_box_complement(const Shape& s, int dtype, int op, const void* src, voi
   void* R = ar.take((size_t)rows * es);
   void* T = ar.take((size_t)rows * es);
   PassPlan p = plan_passes(s, d - 1);  // W = windowed passes along axes 0..d-2
+  if (l2pipe_ok(dtype, op, d, s.ext, s.k) && aligned16(src) && aligned16(dst)) {
+    // R needs all of A before any output row: a reduction pre-pass, the tail
+    // T = BC(R, k[:-1]), then the W passes + row round in one persistent kernel
+    if (live) {
+      ProfScope ps("row_reduce", (double)(s.N + rows) * es, st);
+      *launches += launch_row_reduce(dtype, op, src, R, rows, n, st);
+    }
+    Shape t;
+    t.d = d - 1;
+    t.N = rows;
+    for (int i = 0; i < d - 1; ++i) {
+      t.ext[i] = s.ext[i];
+      t.k[i] = s.k[i];
+    }
+    int rc = route_box_complement(t, dtype, op, R, T, ar, st, launches);
+    if (rc) return rc;
+    void* ws = ar.take(l2pipe_workspace_bytes(s.ext));
+    if (live) {
+      ProfScope ps("l2pipe", (double)(2 * s.N + rows) * es, st);
+      rc = launch_l2pipe(1, src, dst, s.ext, T, ws, st);
+      if (rc < 0) return fail(EXSUM_ECUDA, "L2-pipelined kernel failed to launch");
+      *launches += rc;
+    }
+    return EXSUM_OK;
+  }
   const bool fused = p.count > 0 && p.axes[p.count - 1] == d - 2 &&
                      fused_pair_ok(dtype, op, n, s.k[d - 2], s.k[d - 1], ROW_EXCL) &&
                      aligned16(dst) && (p.count > 1 || aligned16(src));

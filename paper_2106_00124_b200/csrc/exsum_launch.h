@@ -104,6 +104,14 @@ int block_fused_plan(int dtype, int d, const int64_t* ext, const int64_t* k, int
 int launch_block_fused(int dtype, int op, const void* in, void* out, int64_t N, const BlockSpec& bs,
                        const void* total, cudaStream_t s);
 
+// L2-pipelined 3-D schedule (l2pipe.cu; opt-in EXSUM_L2PIPE=1): float32
+// [n0, n1, 1024] with box 16^3 in one persistent kernel -- mode 0 bdbs,
+// mode 1 the box-complement W passes + row round with tail T.
+int l2pipe_ok(int dtype, int op, int d, const int64_t* ext, const int64_t* k);
+size_t l2pipe_workspace_bytes(const int64_t* ext);
+int launch_l2pipe(int mode, const void* in, void* out, const int64_t* ext, const void* Tail,
+                  void* ws, cudaStream_t s);
+
 // ---------------------------------------------- sat / satc / mod-add (sat.cu)
 
 // Inclusive running fold (ops.accumulate: np.add / np.maximum .accumulate)
