@@ -520,9 +520,10 @@ int go_fused(const T* in, T* out, int64_t outer, int64_t n1, int64_t n2, int64_t
     }
   } else {
     // + with a cubic box: row total minus the exact windowed row op (8-byte
-    // elements only for k <= 4: larger windows spill on that path)
+    // elements for k <= 4 or 256-wide rows: larger windows on wider rows spill;
+    // C2 int64 box-complement fused pass 0.084 -> 0.060 ms)
     if constexpr (std::is_same<Op, OpAdd>::value) {
-      if (k2 == k1 && (sizeof(T) == 4 || k1 <= 4)) {
+      if (k2 == k1 && (sizeof(T) == 4 || k1 <= 4 || n2 == 256)) {
         switch (n2) {
           case 256: return pick_k1<T, Op, 8, ROW_EXCL_ADD>(in, out, outer, n1, k1, k2, nullptr, Tail, s);
           case 512: return pick_k1<T, Op, 16, ROW_EXCL_ADD>(in, out, outer, n1, k1, k2, nullptr, Tail, s);
