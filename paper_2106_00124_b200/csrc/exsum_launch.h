@@ -76,7 +76,7 @@ size_t excl_rows_scratch_elems(int dtype, int64_t rows, int64_t n);
 // k1) followed by a row op along n2 -- ROW_WIN: windowed pass with window k2
 // (+ BDBSC epilogue when total != nullptr); ROW_EXCL: box-complement round with
 // shift k2 and tail T (nullable).  fused_pair_ok() decides eligibility.
-enum { ROW_WIN = 0, ROW_EXCL = 1, ROW_EXCL_ADD = 2 /* internal: chosen by go_fused */ };
+enum { ROW_WIN = 0, ROW_EXCL = 1, ROW_EXCL_ADD = 2, ROW_EXCL_BLK = 3 /* 2, 3 internal: chosen by go_fused */ };
 int fused_pair_ok(int dtype, int op, int64_t n2, int64_t k1, int64_t k2, int mode);
 int launch_fused_pair(int dtype, int op, const void* in, void* out, int64_t outer, int64_t n1,
                       int64_t n2, int64_t k1, int64_t k2, int mode, const void* total,

@@ -42,6 +42,9 @@ namespace exsum {
 // K1: window along axis d-2 (compile time); the ROW_WIN row op uses the same
 // window along the row (K2 == K1, the cubic boxes of the BASELINE configs);
 // ROW_EXCL takes any shift kx at run time.
+#ifndef FP_EXCL_BLK
+#define FP_EXCL_BLK 1
+#endif
 #ifndef FP_NARROW_C
 #define FP_NARROW_C 8
 #endif
@@ -326,6 +329,93 @@ k_fused_pair(const T* __restrict__ in, T* __restrict__ out, int64_t outer, int64
             }
             *reinterpret_cast<VT*>(cvec(lane, v)) = q;
           }
+        } else if constexpr (MODE == ROW_EXCL_BLK) {
+          // box-complement row round with kx == K2 (the box is cubic in the
+          // last two axes) and any monoid: the lane chunk holds M2 whole
+          // K2-blocks, and for x at offset r of block j the excluded set
+          // [0, x) u [x+K2, n2) is
+          //   (blocks left of j) (+) p_j[r-1] (+) s_{j+1}[r] (+) (blocks right of j+1)
+          // with p / s the in-block prefix / suffix -- 4 applications per
+          // element instead of the full-row P / S chains' 6 (C2 int64 max:
+          // each is 2 ISETP + 2 SEL).  Reassociated for floats (tolerance,
+          // like ROW_EXCL); exact for max.
+          constexpr int NBV = (K2 + VE - 1) / VE;
+          T nb[NBV * VE];  // next lane's first block, raw (identity past the row)
+#pragma unroll
+          for (int v = 0; v < NBV; ++v) {
+            VT q;
+            if (lane < 31) q = *reinterpret_cast<const VT*>(cvec(lane + 1, v));
+#pragma unroll
+            for (int j = 0; j < VE; ++j) nb[v * VE + j] = lane < 31 ? q.v[j] : ident;
+          }
+          T bt[M2];  // block totals
+#pragma unroll
+          for (int j = 0; j < M2; ++j) {
+            T t0 = a[j * K2], t1 = a[j * K2 + 1];
+#pragma unroll
+            for (int r = 2; r < K2; r += 2) {
+              t0 = Op::apply(t0, a[j * K2 + r]);
+              if (r + 1 < K2) t1 = Op::apply(t1, a[j * K2 + r + 1]);
+            }
+            bt[j] = K2 > 1 ? Op::apply(t0, t1) : t0;
+          }
+          T lt = bt[0];
+#pragma unroll
+          for (int j = 1; j < M2; ++j) lt = Op::apply(lt, bt[j]);
+          // exclusive warp scans of the lane totals
+          T pin = lt, sin = lt;
+#pragma unroll
+          for (int d = 1; d < 32; d <<= 1) {
+            const T tp = __shfl_up_sync(0xffffffffu, pin, d);
+            const T ts = __shfl_down_sync(0xffffffffu, sin, d);
+            if (lane >= d) pin = Op::apply(tp, pin);
+            if (lane + d < 32) sin = Op::apply(sin, ts);
+          }
+          T pre = __shfl_up_sync(0xffffffffu, pin, 1);
+          T suf = __shfl_down_sync(0xffffffffu, sin, 1);
+          if (lane == 0) pre = ident;
+          if (lane == 31) suf = ident;
+          // R[j]: blocks right of block j (in this row)
+          T R[M2];
+          R[M2 - 1] = suf;
+#pragma unroll
+          for (int j = M2 - 2; j >= 0; --j) R[j] = Op::apply(bt[j + 1], R[j + 1]);
+          // blocks right of the next lane's block 0
+          T Rn = __shfl_down_sync(0xffffffffu, R[0], 1);
+          if (lane == 31) Rn = ident;
+          __syncwarp();
+          const T tail = tails[ri];
+          T BP = pre;  // blocks left of block j
+#pragma unroll
+          for (int j = 0; j < M2; ++j) {
+            // in-block suffix of block j+1 (own chunk or the next lane's)
+            T sn[K2];
+            if (j + 1 < M2) {
+              sn[K2 - 1] = a[(j + 1) * K2 + K2 - 1];
+#pragma unroll
+              for (int r = K2 - 2; r >= 0; --r) sn[r] = Op::apply(a[(j + 1) * K2 + r], sn[r + 1]);
+            } else {
+              sn[K2 - 1] = nb[K2 - 1];
+#pragma unroll
+              for (int r = K2 - 2; r >= 0; --r) sn[r] = Op::apply(nb[r], sn[r + 1]);
+            }
+            const T A = Op::apply(Op::apply(BP, j + 1 < M2 ? R[j + 1] : Rn), tail);
+            BP = Op::apply(BP, bt[j]);
+            T run = A;  // A (+) p_j[r-1]
+#pragma unroll
+            for (int r = 0; r < K2; ++r) {
+              const T raw = a[j * K2 + r];
+              a[j * K2 + r] = Op::apply(run, sn[r]);
+              run = Op::apply(run, raw);
+            }
+          }
+#pragma unroll
+          for (int v = 0; v < CV; ++v) {
+            VT q;
+#pragma unroll
+            for (int j = 0; j < VE; ++j) q.v[j] = a[v * VE + j];
+            *reinterpret_cast<VT*>(cvec(lane, v)) = q;
+          }
         } else {
           // full-row prefix / suffix.  The lane chunk is cut into SUB
           // sub-chunks whose folds and scans run as independent chains
@@ -531,6 +621,16 @@ int go_fused(const T* in, T* out, int64_t outer, int64_t n1, int64_t n2, int64_t
             if constexpr (sizeof(T) == 4) return pick_k1<T, Op, 32, ROW_EXCL_ADD>(in, out, outer, n1, k1, k2, nullptr, Tail, s);
             return -1;
         }
+      }
+    }
+    // cubic in the last two axes: the block-decomposed row round (any monoid)
+    if (k2 == k1 && FP_EXCL_BLK) {
+      switch (n2) {
+        case 256: return pick_k1<T, Op, 8, ROW_EXCL_BLK>(in, out, outer, n1, k1, k2, nullptr, Tail, s);
+        case 512: return pick_k1<T, Op, 16, ROW_EXCL_BLK>(in, out, outer, n1, k1, k2, nullptr, Tail, s);
+        case 1024:
+          if constexpr (sizeof(T) == 4) return pick_k1<T, Op, 32, ROW_EXCL_BLK>(in, out, outer, n1, k1, k2, nullptr, Tail, s);
+          return -1;
       }
     }
     switch (n2) {

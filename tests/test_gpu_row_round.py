@@ -1,0 +1,96 @@
+"""GPU parity of the box-complement row round inside the fused pass pair.
+
+The fused pass pair (csrc/fused_pair.cuh) runs the row round of
+box_complement_excluded (excluded.py:151-156 restated, peeled last axis) in
+one of three forms, picked by go_fused:
+  ROW_EXCL_ADD  + with a cubic box in the last two axes (row total - window),
+  ROW_EXCL_BLK  any monoid, cubic in the last two axes (in-block prefix /
+                suffix of the K2-blocks + block-level scans),
+  ROW_EXCL      anything else (full-row prefix / suffix).
+Each form is hit here on the row lengths the pair serves (256, 512, 1024),
+every window it instantiates, ragged axis-(d-2) lengths and several outer
+indices, against the CPU oracle: bit-exact for int64 and max, within the
+reassociation bound of tests/parity.py for floats.
+"""
+
+import numpy as np
+import pytest
+
+from oracle import oracle as orc
+from parity import compare
+
+pytestmark = pytest.mark.gpu
+
+
+@pytest.fixture(scope="module")
+def ex():
+    import torch
+
+    assert torch.cuda.is_available()
+    import paper_2106_00124_b200 as ex
+
+    ex._native.load()
+    return ex
+
+
+def _run(ex, mono, a, box):
+    import torch
+
+    t = ex.Tensor(ex.resolve_monoid(mono), torch.from_numpy(np.ascontiguousarray(a)).cuda())
+    return ex.box_complement_excluded(t, box).data.cpu().numpy()
+
+
+def _data(mono, shape, seed):
+    rng = np.random.default_rng(seed)
+    if mono.endswith("i64"):
+        return rng.integers(-2**40, 2**40, size=shape, dtype=np.int64)
+    dt = np.float32 if mono == "add-f32" else np.float64
+    return rng.standard_normal(shape).astype(dt)
+
+
+CASES = []
+for n2, monos in ((256, ("max-i64", "add-i64", "add-f64", "add-f32")),
+                  (512, ("max-i64", "add-i64", "add-f64", "add-f32")),
+                  (1024, ("add-f32",))):
+    for k in (2, 4, 8, 16):
+        if k == 16 and n2 == 256:
+            continue  # the pair takes k1 = 16 on rows of >= 512
+        for mono in monos:
+            CASES.append((mono, n2, k, k))      # cubic: BLK / ADD
+        CASES.append((monos[0], n2, k, 3))      # k2 != k1: the full-row form
+        CASES.append((monos[0], n2, k, 2 * k))
+
+
+@pytest.mark.parametrize("mono,n2,k1,k2", CASES, ids=lambda v: str(v))
+def test_row_round_forms(ex, mono, n2, k1, k2):
+    n1 = 37 if k1 <= 8 else 70  # ragged: the last k1-block of axis d-2 is partial
+    shape = (3, n1, n2)
+    a = _data(mono, shape, seed=n2 * 100 + k1 * 10 + k2)
+    box = (2, k1, k2)
+    got = _run(ex, mono, a, box)
+    op = "max" if mono.startswith("max") else "add"
+    want = orc.box_complement_excluded(a, box, op)
+    ok, ratio, rel = compare("box-complement", got, want, a, box, orc)
+    assert ok, (mono, shape, box, ratio, rel)
+
+
+@pytest.mark.parametrize("mono", ["max-i64", "add-f64"])
+def test_row_round_extreme_values(ex, mono):
+    """Identity-adjacent values: int64 extremes for max, signed zeros and huge
+    magnitudes for +, on the BLK form (cubic box, 256-wide rows)."""
+    rng = np.random.default_rng(7)
+    shape = (2, 24, 256)
+    if mono == "max-i64":
+        a = rng.choice(np.array([np.iinfo(np.int64).min, np.iinfo(np.int64).max, -1, 0, 1],
+                                dtype=np.int64), size=shape)
+        a[1] = np.iinfo(np.int64).min  # a slab of identities
+    else:
+        a = rng.choice(np.array([0.0, -0.0, 1e300, -1e300, 1.0]), size=shape)
+    box = (1, 8, 8)
+    got = _run(ex, mono, a, box)
+    want = orc.box_complement_excluded(a, box, "max" if mono.startswith("max") else "add")
+    if mono == "max-i64":
+        assert np.array_equal(got, want)
+    else:
+        ok, ratio, rel = compare("box-complement", got, want, a, box, orc)
+        assert ok, (ratio, rel)
