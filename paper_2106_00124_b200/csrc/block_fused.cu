@@ -162,6 +162,132 @@ k_block_fused(const T* __restrict__ in, T* __restrict__ out, int64_t nblocks, Bl
   }
 }
 
+// ---- cubic trailing blocks (every fused axis of length NL, M of them): the
+// same passes with the line length, the strides and the line -> shared-memory
+// map known at compile time.  The line walk unrolls completely -- no bounds
+// tests, shared addresses as immediates off one base, the next block's loads
+// free to issue ahead of the current block's stores -- which the runtime-shape
+// kernel above cannot do (C3d 28^5: 63 thread instructions per element there,
+// issue-bound at 64% busy).  Same association, bit-identical results.
+template <class T, class Op, int K, int N, int ST>
+__device__ __forceinline__ void bf_line_c(T* p) {
+  constexpr int NB = (N + K - 1) / K;
+  T cur[K];
+#pragma unroll
+  for (int r = 0; r < K; ++r)
+    if (r < N) cur[r] = p[r * ST];
+#pragma unroll
+  for (int b = 0; b < NB; ++b) {
+    const int bs = b * K;
+    const int blen = N - bs < K ? N - bs : K;
+#pragma unroll
+    for (int r = K - 2; r >= 0; --r)
+      if (r < blen - 1) cur[r] = Op::apply(cur[r], cur[r + 1]);
+    if (b == NB - 1) {  // last block: out = S
+#pragma unroll
+      for (int r = 0; r < K; ++r)
+        if (r < blen) p[(bs + r) * ST] = cur[r];
+    } else {
+      const int nlen = N - bs - K < K ? N - bs - K : K;
+      T nxt[K];
+#pragma unroll
+      for (int r = 0; r < K; ++r)
+        if (r < nlen) nxt[r] = p[(bs + K + r) * ST];
+      p[bs * ST] = cur[0];
+      T P = nxt[0];
+#pragma unroll
+      for (int r = 1; r < K; ++r) {
+        const int jj = r - 1;
+        if (jj >= 1 && jj < nlen) P = Op::apply(P, nxt[jj]);
+        p[(bs + r) * ST] = Op::apply(cur[r], P);
+      }
+#pragma unroll
+      for (int r = 0; r < K; ++r) cur[r] = nxt[r];
+    }
+  }
+}
+
+__host__ __device__ constexpr int bf_pow(int b, int e) { return e <= 0 ? 1 : b * bf_pow(b, e - 1); }
+
+// the pass along block axis J (0 = outermost of the M fused axes)
+template <class T, class Op, int K, int NL, int M, int J>
+__device__ __forceinline__ void bf_pass_c(T* sm, int lines, int tid, int nt) {
+  constexpr int RP = NL | 1;
+  if constexpr (J == M - 1) {
+    for (int r = tid; r < lines; r += nt) bf_line_c<T, Op, K, NL, 1>(sm + r * RP);
+  } else {
+    constexpr int INNER = bf_pow(NL, M - 1 - J);  // valid elements after axis J
+    constexpr int INNER_P = INNER / NL * RP;      // padded stride of axis J
+    for (int L = tid; L < lines; L += nt) {
+      const int o = L / INNER;
+      const int i = L - o * INNER;
+      const int ir = i / NL;
+      bf_line_c<T, Op, K, NL, INNER_P>(sm + (o * NL * INNER_P + ir * RP + (i - ir * NL)));
+    }
+  }
+}
+
+template <class T, class Op, int K, int NL, int M, bool VEC>
+__global__ void __launch_bounds__(512)
+k_block_cubic(const T* __restrict__ in, T* __restrict__ out, int64_t nblocks, int G, int passes,
+              const typename AccOf<T>::type* __restrict__ total) {
+  constexpr int VE = 16 / sizeof(T);
+  constexpr int RP = NL | 1;
+  constexpr int B = bf_pow(NL, M);
+  extern __shared__ __align__(16) unsigned char smem[];
+  T* sm = reinterpret_cast<T*>(smem);
+  const int tid = threadIdx.x;
+  const int nt = blockDim.x;
+  const T tot = total ? (T)(*total) : T(0);
+  const bool epi = total != nullptr;
+  const int64_t ntiles = (nblocks + G - 1) / G;
+  for (int64_t tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
+    const int64_t b0 = tile * G;
+    const int g = (int)(nblocks - b0 < G ? nblocks - b0 : G);
+    const int E = g * B;
+    const T* src = in + b0 * B;
+    T* dst = out + b0 * B;
+    for (int e = tid; e < E; e += nt) {
+      const int row = e / NL;
+      cp_async_n<sizeof(T)>(sm + row * RP + (e - row * NL), src + e);
+    }
+    cp_async_commit();
+    cp_async_wait<0>();
+    __syncthreads();
+    const int lines = E / NL;
+    // passes: bit j set = axis j of the block has a window (> 1)
+    if (passes & 1) { bf_pass_c<T, Op, K, NL, M, 0>(sm, lines, tid, nt); __syncthreads(); }
+    if (passes & 2) { bf_pass_c<T, Op, K, NL, M, 1>(sm, lines, tid, nt); __syncthreads(); }
+    if constexpr (M > 2) {
+      if (passes & 4) { bf_pass_c<T, Op, K, NL, M, 2 % M>(sm, lines, tid, nt); __syncthreads(); }
+    }
+    if constexpr (VEC) {
+      for (int e = tid * VE; e < E; e += nt * VE) {
+        Vec<T, VE> v;
+        int row = e / NL;
+        int col = e - row * NL;
+#pragma unroll
+        for (int j = 0; j < VE; ++j) {
+          const T w = sm[row * RP + col];
+          v.v[j] = epi ? OpAdd::inverse<T>(tot, w) : w;
+          if (++col == NL) {
+            col = 0;
+            ++row;
+          }
+        }
+        st_stream<T, VE>(dst + e, v);
+      }
+    } else {
+      for (int e = tid; e < E; e += nt) {
+        const int row = e / NL;
+        const T w = sm[row * RP + (e - row * NL)];
+        st1(dst + e, epi ? OpAdd::inverse<T>(tot, w) : w);
+      }
+    }
+    __syncthreads();
+  }
+}
+
 static uint32_t bf_magic(uint32_t d) {
   // ceil(2^32 / d): exact quotients for x < 2^32 / d; 0 marks d == 1
   return d <= 1 ? 0u : (uint32_t)((((uint64_t)1 << 32) + d - 1) / d);
@@ -231,9 +357,53 @@ int block_fused_plan(int dtype, int d, const int64_t* ext, const int64_t* k, int
   return 0;
 }
 
+template <class T, class Op, int K, int NL, int M>
+static int go_cubic(const T* in, T* out, int64_t N, const BlockSpec& bs,
+                    const typename AccOf<T>::type* total, cudaStream_t s) {
+  const int64_t nblocks = N / bs.B;
+  int passes = 0;
+  for (int j = 0; j < M; ++j)
+    if (bs.k[j] > 1) passes |= 1 << j;
+  // threads: the tile's lines in as few equal rounds as 512 threads allow
+  const int64_t lines = (int64_t)bs.G * bs.B / NL;
+  const int64_t rounds = (lines + 511) / 512;
+  int nt = (int)(((lines + rounds - 1) / rounds + 31) / 32 * 32);
+  if (nt < 64) nt = 64;
+  int per_sm = (int)((228 * 1024) / (bs.smem + 1024));
+  if (per_sm > 2048 / nt) per_sm = 2048 / nt;
+  if (per_sm > 32) per_sm = 32;
+  if (per_sm < 1) per_sm = 1;
+  const int64_t ntiles = (nblocks + bs.G - 1) / bs.G;
+  int64_t grid = (int64_t)num_sms() * per_sm;
+  if (grid > ntiles) grid = ntiles;
+  const bool vec = ((uintptr_t)in % 16 == 0) && ((uintptr_t)out % 16 == 0) &&
+                   ((bs.B * (int64_t)sizeof(T)) % 16 == 0);
+  if (vec) {
+    ensure_smem((const void*)k_block_cubic<T, Op, K, NL, M, true>, bs.smem);
+    k_block_cubic<T, Op, K, NL, M, true><<<(unsigned)grid, nt, bs.smem, s>>>(in, out, nblocks, bs.G,
+                                                                             passes, total);
+  } else {
+    ensure_smem((const void*)k_block_cubic<T, Op, K, NL, M, false>, bs.smem);
+    k_block_cubic<T, Op, K, NL, M, false><<<(unsigned)grid, nt, bs.smem, s>>>(in, out, nblocks, bs.G,
+                                                                              passes, total);
+  }
+  return 1;
+}
+
 template <class T, class Op, int K>
 static int go_block(const T* in, T* out, int64_t N, const BlockSpec& bs,
                     const typename AccOf<T>::type* total, cudaStream_t s) {
+  // cubic blocks of the dimension sweep's shapes: the compile-time kernel
+  bool cubic = bf_env("EXSUM_BF_CUBIC", 1) != 0 && (bs.m == 2 || bs.m == 3);
+  for (int j = 1; j < bs.m; ++j) cubic = cubic && bs.n[j] == bs.n[0];
+  if (cubic) {
+    const int nl = bs.n[0];
+    if (bs.m == 3 && nl == 16) return go_cubic<T, Op, K, 16, 3>(in, out, N, bs, total, s);
+    if (bs.m == 3 && nl == 28) return go_cubic<T, Op, K, 28, 3>(in, out, N, bs, total, s);
+    if (bs.m == 2 && nl == 28) return go_cubic<T, Op, K, 28, 2>(in, out, N, bs, total, s);
+    if (bs.m == 2 && nl == 32) return go_cubic<T, Op, K, 32, 2>(in, out, N, bs, total, s);
+    if (bs.m == 2 && nl == 64) return go_cubic<T, Op, K, 64, 2>(in, out, N, bs, total, s);
+  }
   const int64_t nblocks = N / bs.B;
   int per_sm = (int)((228 * 1024) / (bs.smem + 1024));
   if (per_sm > 2048 / bs.threads) per_sm = 2048 / bs.threads;
