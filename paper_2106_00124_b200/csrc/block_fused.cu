@@ -209,12 +209,79 @@ __device__ __forceinline__ void bf_line_c(T* p) {
 
 __host__ __device__ constexpr int bf_pow(int b, int e) { return e <= 0 ? 1 : b * bf_pow(b, e - 1); }
 
+// the same walk over a line held in registers (the row pass: a thread loads
+// its row as 16-byte vectors, walks it, stores it back as vectors)
+template <class T, class Op, int K, int N>
+__device__ __forceinline__ void bf_line_r(T (&v)[N]) {
+  constexpr int NB = (N + K - 1) / K;
+  T cur[K];
+#pragma unroll
+  for (int r = 0; r < K; ++r)
+    if (r < N) cur[r] = v[r];
+#pragma unroll
+  for (int b = 0; b < NB; ++b) {
+    const int bs = b * K;
+    const int blen = N - bs < K ? N - bs : K;
+#pragma unroll
+    for (int r = K - 2; r >= 0; --r)
+      if (r < blen - 1) cur[r] = Op::apply(cur[r], cur[r + 1]);
+    if (b == NB - 1) {
+#pragma unroll
+      for (int r = 0; r < K; ++r)
+        if (r < blen) v[bs + r] = cur[r];
+    } else {
+      const int nlen = N - bs - K < K ? N - bs - K : K;
+      T nxt[K];
+#pragma unroll
+      for (int r = 0; r < K; ++r)
+        if (r < nlen) nxt[r] = v[bs + K + r];
+      v[bs] = cur[0];
+      T P = nxt[0];
+#pragma unroll
+      for (int r = 1; r < K; ++r) {
+        const int jj = r - 1;
+        if (jj >= 1 && jj < nlen) P = Op::apply(P, nxt[jj]);
+        v[bs + r] = Op::apply(cur[r], P);
+      }
+#pragma unroll
+      for (int r = 0; r < K; ++r) cur[r] = nxt[r];
+    }
+  }
+}
+
+// padded row length of the cubic stage: whole 16-byte vectors, an odd number
+// of them -- a thread's row as LDS.128 / STS.128 hits 8 distinct 16-byte bank
+// groups per quarter warp, and rows start 16-byte aligned so the stage fills
+// with 16-byte cp.async copies (float32 rows of 28 need no padding at all)
+__host__ __device__ constexpr int bf_rp(int nl, int ve) {
+  return (((nl + ve - 1) / ve) % 2 == 0 ? (nl + ve - 1) / ve + 1 : (nl + ve - 1) / ve) * ve;
+}
+
 // the pass along block axis J (0 = outermost of the M fused axes)
 template <class T, class Op, int K, int NL, int M, int J>
 __device__ __forceinline__ void bf_pass_c(T* sm, int lines, int tid, int nt) {
-  constexpr int RP = NL | 1;
+  constexpr int VE = 16 / sizeof(T);
+  constexpr int RP = bf_rp(NL, VE);
   if constexpr (J == M - 1) {
-    for (int r = tid; r < lines; r += nt) bf_line_c<T, Op, K, NL, 1>(sm + r * RP);
+    typedef Vec<T, VE> VT;
+    for (int r = tid; r < lines; r += nt) {
+      T v[NL];
+      VT* row = reinterpret_cast<VT*>(sm + r * RP);
+#pragma unroll
+      for (int q = 0; q < NL / VE; ++q) {
+        const VT t = row[q];
+#pragma unroll
+        for (int j = 0; j < VE; ++j) v[q * VE + j] = t.v[j];
+      }
+      bf_line_r<T, Op, K, NL>(v);
+#pragma unroll
+      for (int q = 0; q < NL / VE; ++q) {
+        VT t;
+#pragma unroll
+        for (int j = 0; j < VE; ++j) t.v[j] = v[q * VE + j];
+        row[q] = t;
+      }
+    }
   } else {
     constexpr int INNER = bf_pow(NL, M - 1 - J);  // valid elements after axis J
     constexpr int INNER_P = INNER / NL * RP;      // padded stride of axis J
@@ -227,13 +294,15 @@ __device__ __forceinline__ void bf_pass_c(T* sm, int lines, int tid, int nt) {
   }
 }
 
-template <class T, class Op, int K, int NL, int M, bool VEC>
+template <class T, class Op, int K, int NL, int M>
 __global__ void __launch_bounds__(512)
 k_block_cubic(const T* __restrict__ in, T* __restrict__ out, int64_t nblocks, int G, int passes,
               const typename AccOf<T>::type* __restrict__ total) {
   constexpr int VE = 16 / sizeof(T);
-  constexpr int RP = NL | 1;
+  constexpr int RP = bf_rp(NL, VE);
   constexpr int B = bf_pow(NL, M);
+  static_assert(NL % VE == 0, "rows of whole 16-byte vectors");
+  typedef Vec<T, VE> VT;
   extern __shared__ __align__(16) unsigned char smem[];
   T* sm = reinterpret_cast<T*>(smem);
   const int tid = threadIdx.x;
@@ -247,9 +316,10 @@ k_block_cubic(const T* __restrict__ in, T* __restrict__ out, int64_t nblocks, in
     const int E = g * B;
     const T* src = in + b0 * B;
     T* dst = out + b0 * B;
-    for (int e = tid; e < E; e += nt) {
+    // stage in: 16-byte cp.async copies into the padded rows
+    for (int e = tid * VE; e < E; e += nt * VE) {
       const int row = e / NL;
-      cp_async_n<sizeof(T)>(sm + row * RP + (e - row * NL), src + e);
+      cp_async_n<16>(sm + row * RP + (e - row * NL), src + e);
     }
     cp_async_commit();
     cp_async_wait<0>();
@@ -261,28 +331,15 @@ k_block_cubic(const T* __restrict__ in, T* __restrict__ out, int64_t nblocks, in
     if constexpr (M > 2) {
       if (passes & 4) { bf_pass_c<T, Op, K, NL, M, 2 % M>(sm, lines, tid, nt); __syncthreads(); }
     }
-    if constexpr (VEC) {
-      for (int e = tid * VE; e < E; e += nt * VE) {
-        Vec<T, VE> v;
-        int row = e / NL;
-        int col = e - row * NL;
+    // stage out (+ BDBSC complement): 16-byte shared loads, streaming stores
+    for (int e = tid * VE; e < E; e += nt * VE) {
+      const int row = e / NL;
+      VT v = *reinterpret_cast<const VT*>(sm + row * RP + (e - row * NL));
+      if (epi) {
 #pragma unroll
-        for (int j = 0; j < VE; ++j) {
-          const T w = sm[row * RP + col];
-          v.v[j] = epi ? OpAdd::inverse<T>(tot, w) : w;
-          if (++col == NL) {
-            col = 0;
-            ++row;
-          }
-        }
-        st_stream<T, VE>(dst + e, v);
+        for (int j = 0; j < VE; ++j) v.v[j] = OpAdd::inverse<T>(tot, v.v[j]);
       }
-    } else {
-      for (int e = tid; e < E; e += nt) {
-        const int row = e / NL;
-        const T w = sm[row * RP + (e - row * NL)];
-        st1(dst + e, epi ? OpAdd::inverse<T>(tot, w) : w);
-      }
+      st_stream<T, VE>(dst + e, v);
     }
     __syncthreads();
   }
@@ -360,34 +417,34 @@ int block_fused_plan(int dtype, int d, const int64_t* ext, const int64_t* k, int
 template <class T, class Op, int K, int NL, int M>
 static int go_cubic(const T* in, T* out, int64_t N, const BlockSpec& bs,
                     const typename AccOf<T>::type* total, cudaStream_t s) {
-  const int64_t nblocks = N / bs.B;
-  int passes = 0;
-  for (int j = 0; j < M; ++j)
-    if (bs.k[j] > 1) passes |= 1 << j;
-  // threads: the tile's lines in as few equal rounds as 512 threads allow
-  const int64_t lines = (int64_t)bs.G * bs.B / NL;
-  const int64_t rounds = (lines + 511) / 512;
-  int nt = (int)(((lines + rounds - 1) / rounds + 31) / 32 * 32);
-  if (nt < 64) nt = 64;
-  int per_sm = (int)((228 * 1024) / (bs.smem + 1024));
-  if (per_sm > 2048 / nt) per_sm = 2048 / nt;
-  if (per_sm > 32) per_sm = 32;
-  if (per_sm < 1) per_sm = 1;
-  const int64_t ntiles = (nblocks + bs.G - 1) / bs.G;
-  int64_t grid = (int64_t)num_sms() * per_sm;
-  if (grid > ntiles) grid = ntiles;
-  const bool vec = ((uintptr_t)in % 16 == 0) && ((uintptr_t)out % 16 == 0) &&
-                   ((bs.B * (int64_t)sizeof(T)) % 16 == 0);
-  if (vec) {
-    ensure_smem((const void*)k_block_cubic<T, Op, K, NL, M, true>, bs.smem);
-    k_block_cubic<T, Op, K, NL, M, true><<<(unsigned)grid, nt, bs.smem, s>>>(in, out, nblocks, bs.G,
-                                                                             passes, total);
+  constexpr int VE = 16 / sizeof(T);
+  if constexpr (NL % VE != 0) {
+    return 0;
   } else {
-    ensure_smem((const void*)k_block_cubic<T, Op, K, NL, M, false>, bs.smem);
-    k_block_cubic<T, Op, K, NL, M, false><<<(unsigned)grid, nt, bs.smem, s>>>(in, out, nblocks, bs.G,
-                                                                              passes, total);
+    if (((uintptr_t)in % 16) || ((uintptr_t)out % 16)) return 0;  // the runtime-shape kernel
+    const int64_t nblocks = N / bs.B;
+    int passes = 0;
+    for (int j = 0; j < M; ++j)
+      if (bs.k[j] > 1) passes |= 1 << j;
+    const size_t smem = (size_t)bs.G * (bs.B / NL) * bf_rp(NL, VE) * sizeof(T);
+    if (smem > 200 * 1024) return 0;
+    // threads: the tile's lines in as few equal rounds as 512 threads allow
+    const int64_t lines = (int64_t)bs.G * bs.B / NL;
+    const int64_t rounds = (lines + 511) / 512;
+    int nt = (int)(((lines + rounds - 1) / rounds + 31) / 32 * 32);
+    if (nt < 64) nt = 64;
+    int per_sm = (int)((228 * 1024) / (smem + 1024));
+    if (per_sm > 2048 / nt) per_sm = 2048 / nt;
+    if (per_sm > 32) per_sm = 32;
+    if (per_sm < 1) per_sm = 1;
+    const int64_t ntiles = (nblocks + bs.G - 1) / bs.G;
+    int64_t grid = (int64_t)num_sms() * per_sm;
+    if (grid > ntiles) grid = ntiles;
+    ensure_smem((const void*)k_block_cubic<T, Op, K, NL, M>, smem);
+    k_block_cubic<T, Op, K, NL, M><<<(unsigned)grid, nt, smem, s>>>(in, out, nblocks, bs.G, passes,
+                                                                    total);
+    return 1;
   }
-  return 1;
 }
 
 template <class T, class Op, int K>
@@ -398,11 +455,13 @@ static int go_block(const T* in, T* out, int64_t N, const BlockSpec& bs,
   for (int j = 1; j < bs.m; ++j) cubic = cubic && bs.n[j] == bs.n[0];
   if (cubic) {
     const int nl = bs.n[0];
-    if (bs.m == 3 && nl == 16) return go_cubic<T, Op, K, 16, 3>(in, out, N, bs, total, s);
-    if (bs.m == 3 && nl == 28) return go_cubic<T, Op, K, 28, 3>(in, out, N, bs, total, s);
-    if (bs.m == 2 && nl == 28) return go_cubic<T, Op, K, 28, 2>(in, out, N, bs, total, s);
-    if (bs.m == 2 && nl == 32) return go_cubic<T, Op, K, 32, 2>(in, out, N, bs, total, s);
-    if (bs.m == 2 && nl == 64) return go_cubic<T, Op, K, 64, 2>(in, out, N, bs, total, s);
+    int rc = 0;
+    if (bs.m == 3 && nl == 16) rc = go_cubic<T, Op, K, 16, 3>(in, out, N, bs, total, s);
+    if (bs.m == 3 && nl == 28) rc = go_cubic<T, Op, K, 28, 3>(in, out, N, bs, total, s);
+    if (bs.m == 2 && nl == 28) rc = go_cubic<T, Op, K, 28, 2>(in, out, N, bs, total, s);
+    if (bs.m == 2 && nl == 32) rc = go_cubic<T, Op, K, 32, 2>(in, out, N, bs, total, s);
+    if (bs.m == 2 && nl == 64) rc = go_cubic<T, Op, K, 64, 2>(in, out, N, bs, total, s);
+    if (rc) return rc;
   }
   const int64_t nblocks = N / bs.B;
   int per_sm = (int)((228 * 1024) / (bs.smem + 1024));
