@@ -169,13 +169,13 @@ k_block_fused(const T* __restrict__ in, T* __restrict__ out, int64_t nblocks, Bl
 // free to issue ahead of the current block's stores -- which the runtime-shape
 // kernel above cannot do (C3d 28^5: 63 thread instructions per element there,
 // issue-bound at 64% busy).  Same association, bit-identical results.
-template <class T, class Op, int K, int N, int ST>
-__device__ __forceinline__ void bf_line_c(T* p) {
+template <class T, class Op, int K, int N, class At>
+__device__ __forceinline__ void bf_line_c(At at) {
   constexpr int NB = (N + K - 1) / K;
   T cur[K];
 #pragma unroll
   for (int r = 0; r < K; ++r)
-    if (r < N) cur[r] = p[r * ST];
+    if (r < N) cur[r] = *at(r);
 #pragma unroll
   for (int b = 0; b < NB; ++b) {
     const int bs = b * K;
@@ -186,20 +186,20 @@ __device__ __forceinline__ void bf_line_c(T* p) {
     if (b == NB - 1) {  // last block: out = S
 #pragma unroll
       for (int r = 0; r < K; ++r)
-        if (r < blen) p[(bs + r) * ST] = cur[r];
+        if (r < blen) *at(bs + r) = cur[r];
     } else {
       const int nlen = N - bs - K < K ? N - bs - K : K;
       T nxt[K];
 #pragma unroll
       for (int r = 0; r < K; ++r)
-        if (r < nlen) nxt[r] = p[(bs + K + r) * ST];
-      p[bs * ST] = cur[0];
+        if (r < nlen) nxt[r] = *at(bs + K + r);
+      *at(bs) = cur[0];
       T P = nxt[0];
 #pragma unroll
       for (int r = 1; r < K; ++r) {
         const int jj = r - 1;
         if (jj >= 1 && jj < nlen) P = Op::apply(P, nxt[jj]);
-        p[(bs + r) * ST] = Op::apply(cur[r], P);
+        *at(bs + r) = Op::apply(cur[r], P);
       }
 #pragma unroll
       for (int r = 0; r < K; ++r) cur[r] = nxt[r];
@@ -257,19 +257,34 @@ __host__ __device__ constexpr int bf_rp(int nl, int ve) {
   return (((nl + ve - 1) / ve) % 2 == 0 ? (nl + ve - 1) / ve + 1 : (nl + ve - 1) / ve) * ve;
 }
 
+// rows of exactly 4 vectors (float32 rows of 16: the 16^6 sweep) are not
+// padded but XOR-swizzled: vector q of row r sits at q ^ ((r >> 1) & 3).  The
+// row pass (a quarter warp on 8 rows, one vector each) then hits 8 distinct
+// bank groups, and a warp on 32 consecutive columns (two whole rows) stays
+// conflict-free -- the padded 20-wide rows conflicted 2-way there.
+template <int NL, int VE>
+struct BfLayout {
+  static constexpr int V = NL / VE;
+  static constexpr bool SWZ = V == 4;
+  static constexpr int RP = SWZ ? NL : bf_rp(NL, VE);
+  __device__ static __forceinline__ int sw(int row) { return SWZ ? (row >> 1) & 3 : 0; }
+  // shared offset of vector q of row `row`
+  __device__ static __forceinline__ int vec_at(int row, int q) { return row * RP + (q ^ sw(row)) * VE; }
+};
+
 // the pass along block axis J (0 = outermost of the M fused axes)
 template <class T, class Op, int K, int NL, int M, int J>
 __device__ __forceinline__ void bf_pass_c(T* sm, int lines, int tid, int nt) {
   constexpr int VE = 16 / sizeof(T);
-  constexpr int RP = bf_rp(NL, VE);
+  typedef BfLayout<NL, VE> Lay;
+  constexpr int RP = Lay::RP;
   if constexpr (J == M - 1) {
     typedef Vec<T, VE> VT;
     for (int r = tid; r < lines; r += nt) {
       T v[NL];
-      VT* row = reinterpret_cast<VT*>(sm + r * RP);
 #pragma unroll
       for (int q = 0; q < NL / VE; ++q) {
-        const VT t = row[q];
+        const VT t = *reinterpret_cast<const VT*>(sm + Lay::vec_at(r, q));
 #pragma unroll
         for (int j = 0; j < VE; ++j) v[q * VE + j] = t.v[j];
       }
@@ -279,17 +294,31 @@ __device__ __forceinline__ void bf_pass_c(T* sm, int lines, int tid, int nt) {
         VT t;
 #pragma unroll
         for (int j = 0; j < VE; ++j) t.v[j] = v[q * VE + j];
-        row[q] = t;
+        *reinterpret_cast<VT*>(sm + Lay::vec_at(r, q)) = t;
       }
     }
   } else {
     constexpr int INNER = bf_pow(NL, M - 1 - J);  // valid elements after axis J
-    constexpr int INNER_P = INNER / NL * RP;      // padded stride of axis J
+    constexpr int RSTEP = INNER / NL;             // rows per step along axis J
+    constexpr int INNER_P = RSTEP * RP;           // padded stride of axis J
     for (int L = tid; L < lines; L += nt) {
       const int o = L / INNER;
       const int i = L - o * INNER;
       const int ir = i / NL;
-      bf_line_c<T, Op, K, NL, INNER_P>(sm + (o * NL * INNER_P + ir * RP + (i - ir * NL)));
+      const int c = i - ir * NL;
+      const int row0 = o * NL * RSTEP + ir;
+      if constexpr (Lay::SWZ && RSTEP == 1) {
+        // rows advance by one along the line and row0 is a multiple of NL:
+        // the swizzle of row0 + r is (r >> 1) & 3, known at compile time
+        T* bt[4];
+#pragma unroll
+        for (int t = 0; t < 4; ++t) bt[t] = sm + row0 * RP + ((c / VE) ^ t) * VE + c % VE;
+        bf_line_c<T, Op, K, NL>([&](int r) { return bt[(r >> 1) & 3] + r * RP; });
+      } else {
+        // rows advance by multiples of 16 (or no swizzle): one column offset
+        T* p = sm + row0 * RP + ((c / VE) ^ Lay::sw(row0)) * VE + c % VE;
+        bf_line_c<T, Op, K, NL>([&](int r) { return p + r * INNER_P; });
+      }
     }
   }
 }
@@ -299,9 +328,10 @@ __global__ void __launch_bounds__(512)
 k_block_cubic(const T* __restrict__ in, T* __restrict__ out, int64_t nblocks, int G, int passes,
               const typename AccOf<T>::type* __restrict__ total) {
   constexpr int VE = 16 / sizeof(T);
-  constexpr int RP = bf_rp(NL, VE);
+  typedef BfLayout<NL, VE> Lay;
   constexpr int B = bf_pow(NL, M);
   static_assert(NL % VE == 0, "rows of whole 16-byte vectors");
+  static_assert(!Lay::SWZ || NL % 16 == 0, "the swizzle assumes row0 % 8 == 0 per line");
   typedef Vec<T, VE> VT;
   extern __shared__ __align__(16) unsigned char smem[];
   T* sm = reinterpret_cast<T*>(smem);
@@ -319,7 +349,7 @@ k_block_cubic(const T* __restrict__ in, T* __restrict__ out, int64_t nblocks, in
     // stage in: 16-byte cp.async copies into the padded rows
     for (int e = tid * VE; e < E; e += nt * VE) {
       const int row = e / NL;
-      cp_async_n<16>(sm + row * RP + (e - row * NL), src + e);
+      cp_async_n<16>(sm + Lay::vec_at(row, (e - row * NL) / VE), src + e);
     }
     cp_async_commit();
     cp_async_wait<0>();
@@ -334,7 +364,7 @@ k_block_cubic(const T* __restrict__ in, T* __restrict__ out, int64_t nblocks, in
     // stage out (+ BDBSC complement): 16-byte shared loads, streaming stores
     for (int e = tid * VE; e < E; e += nt * VE) {
       const int row = e / NL;
-      VT v = *reinterpret_cast<const VT*>(sm + row * RP + (e - row * NL));
+      VT v = *reinterpret_cast<const VT*>(sm + Lay::vec_at(row, (e - row * NL) / VE));
       if (epi) {
 #pragma unroll
         for (int j = 0; j < VE; ++j) v.v[j] = OpAdd::inverse<T>(tot, v.v[j]);
@@ -426,7 +456,7 @@ static int go_cubic(const T* in, T* out, int64_t N, const BlockSpec& bs,
     int passes = 0;
     for (int j = 0; j < M; ++j)
       if (bs.k[j] > 1) passes |= 1 << j;
-    const size_t smem = (size_t)bs.G * (bs.B / NL) * bf_rp(NL, VE) * sizeof(T);
+    const size_t smem = (size_t)bs.G * (bs.B / NL) * BfLayout<NL, VE>::RP * sizeof(T);
     if (smem > 200 * 1024) return 0;
     // threads: the tile's lines in as few equal rounds as 512 threads allow
     const int64_t lines = (int64_t)bs.G * bs.B / NL;
