@@ -262,21 +262,31 @@ __host__ __device__ constexpr int bf_rp(int nl, int ve) {
 // row pass (a quarter warp on 8 rows, one vector each) then hits 8 distinct
 // bank groups, and a warp on 32 consecutive columns (two whole rows) stays
 // conflict-free -- the padded 20-wide rows conflicted 2-way there.
-template <int NL, int VE>
+// Planes (the NL rows of one index of the block's axis M-2) are padded to a
+// stride PS = NL (mod 128 bytes): a warp on 32 consecutive lines of the axis
+// M-2 pass (columns of consecutive planes) then lands on 32 consecutive
+// bank words -- unpadded 28 x 28 planes (784 = 16 mod 32 words) put two
+// planes' columns on the same banks.
+template <class T, int NL>
 struct BfLayout {
+  static constexpr int VE = 16 / sizeof(T);
+  static constexpr int W = 128 / sizeof(T);  // elements per 128-byte bank row
   static constexpr int V = NL / VE;
   static constexpr bool SWZ = V == 4;
   static constexpr int RP = SWZ ? NL : bf_rp(NL, VE);
+  static constexpr int PLANE = NL * RP;
+  static constexpr int PS = PLANE + ((NL - PLANE) % W + W) % W;
   __device__ static __forceinline__ int sw(int row) { return SWZ ? (row >> 1) & 3 : 0; }
+  __device__ static __forceinline__ int row_at(int row) { return (row / NL) * PS + (row % NL) * RP; }
   // shared offset of vector q of row `row`
-  __device__ static __forceinline__ int vec_at(int row, int q) { return row * RP + (q ^ sw(row)) * VE; }
+  __device__ static __forceinline__ int vec_at(int row, int q) { return row_at(row) + (q ^ sw(row)) * VE; }
 };
 
 // the pass along block axis J (0 = outermost of the M fused axes)
 template <class T, class Op, int K, int NL, int M, int J>
 __device__ __forceinline__ void bf_pass_c(T* sm, int lines, int tid, int nt) {
   constexpr int VE = 16 / sizeof(T);
-  typedef BfLayout<NL, VE> Lay;
+  typedef BfLayout<T, NL> Lay;
   constexpr int RP = Lay::RP;
   if constexpr (J == M - 1) {
     typedef Vec<T, VE> VT;
@@ -300,7 +310,8 @@ __device__ __forceinline__ void bf_pass_c(T* sm, int lines, int tid, int nt) {
   } else {
     constexpr int INNER = bf_pow(NL, M - 1 - J);  // valid elements after axis J
     constexpr int RSTEP = INNER / NL;             // rows per step along axis J
-    constexpr int INNER_P = RSTEP * RP;           // padded stride of axis J
+    // element stride of axis J: one row (J = M-2) or whole planes
+    constexpr int INNER_P = RSTEP == 1 ? RP : (RSTEP / NL) * Lay::PS;
     for (int L = tid; L < lines; L += nt) {
       const int o = L / INNER;
       const int i = L - o * INNER;
@@ -312,11 +323,11 @@ __device__ __forceinline__ void bf_pass_c(T* sm, int lines, int tid, int nt) {
         // the swizzle of row0 + r is (r >> 1) & 3, known at compile time
         T* bt[4];
 #pragma unroll
-        for (int t = 0; t < 4; ++t) bt[t] = sm + row0 * RP + ((c / VE) ^ t) * VE + c % VE;
+        for (int t = 0; t < 4; ++t) bt[t] = sm + Lay::row_at(row0) + ((c / VE) ^ t) * VE + c % VE;
         bf_line_c<T, Op, K, NL>([&](int r) { return bt[(r >> 1) & 3] + r * RP; });
       } else {
         // rows advance by multiples of 16 (or no swizzle): one column offset
-        T* p = sm + row0 * RP + ((c / VE) ^ Lay::sw(row0)) * VE + c % VE;
+        T* p = sm + Lay::row_at(row0) + ((c / VE) ^ Lay::sw(row0)) * VE + c % VE;
         bf_line_c<T, Op, K, NL>([&](int r) { return p + r * INNER_P; });
       }
     }
@@ -328,7 +339,7 @@ __global__ void __launch_bounds__(512)
 k_block_cubic(const T* __restrict__ in, T* __restrict__ out, int64_t nblocks, int G, int passes,
               const typename AccOf<T>::type* __restrict__ total) {
   constexpr int VE = 16 / sizeof(T);
-  typedef BfLayout<NL, VE> Lay;
+  typedef BfLayout<T, NL> Lay;
   constexpr int B = bf_pow(NL, M);
   static_assert(NL % VE == 0, "rows of whole 16-byte vectors");
   static_assert(!Lay::SWZ || NL % 16 == 0, "the swizzle assumes row0 % 8 == 0 per line");
@@ -456,7 +467,7 @@ static int go_cubic(const T* in, T* out, int64_t N, const BlockSpec& bs,
     int passes = 0;
     for (int j = 0; j < M; ++j)
       if (bs.k[j] > 1) passes |= 1 << j;
-    const size_t smem = (size_t)bs.G * (bs.B / NL) * BfLayout<NL, VE>::RP * sizeof(T);
+    const size_t smem = (size_t)bs.G * (bs.B / NL / NL) * BfLayout<T, NL>::PS * sizeof(T);
     if (smem > 200 * 1024) return 0;
     // threads: the tile's lines in as few equal rounds as 512 threads allow
     const int64_t lines = (int64_t)bs.G * bs.B / NL;
