@@ -121,3 +121,59 @@ def test_block_fused_is_taken_for_c3_shapes(ex, mono):
         ref, n_plain = _run(ex, "bdbs", mono, a, box, fuse=0)
         assert _bits_equal(got, ref), shape
         assert n_fused < n_plain, (shape, n_fused, n_plain)
+
+
+def _run_env(ex, route, mono, arr, box, env):
+    old = {k: os.environ.get(k) for k in env}
+    os.environ.update(env)
+    try:
+        return _run(ex, route, mono, arr, box, fuse=1)
+    finally:
+        for k, v in old.items():
+            if v is None:
+                del os.environ[k]
+            else:
+                os.environ[k] = v
+
+
+# cubic trailing blocks take k_block_cubic<NL, M> (compile-time line length,
+# strides and layout: odd vector stride, XOR-swizzled 64-byte rows, padded
+# planes); every NL / M form, every window, skipped axes (k = 1) inside the
+# block, tiles of several blocks, against the oracle and the runtime-shape
+# kernel (EXSUM_BF_CUBIC=0)
+# leading extents large enough that the plan stops at the cubic block (a
+# small leading axis would join the block and take the runtime-shape kernel)
+CUBIC = [
+    ((7, 16, 16, 16), (2, 2, 2, 2)),
+    ((7, 16, 16, 16), (4, 1, 4, 4)),
+    ((2, 16, 16, 16, 16), (4, 4, 4, 1, 4)),
+    ((4, 28, 28, 28), (4, 4, 4, 4)),
+    ((4, 28, 28, 28), (2, 2, 1, 2)),
+    ((200, 28, 28), (4, 4, 4)),
+    ((120, 32, 32), (2, 2, 2)),
+    ((120, 32, 32), (4, 4, 4)),
+    ((9, 64, 64), (4, 4, 4)),
+    ((9, 64, 64), (2, 2, 1)),
+    ((3, 28, 28, 28), (8, 8, 8, 8)),
+    ((7, 16, 16, 16), (8, 8, 8, 8)),
+]
+
+
+@pytest.mark.parametrize("shape,box", CUBIC, ids=lambda v: "x".join(map(str, v)))
+@pytest.mark.parametrize("mono", ["add-f32", "add-i64", "max-i64", "add-f64"])
+def test_block_cubic_forms(ex, shape, box, mono):
+    rng = np.random.default_rng(11 * sum(shape) + sum(box) + len(mono))
+    a = _data(rng, mono, shape)
+    op = "max" if mono == "max-i64" else "add"
+    want = orc.ROUTES["bdbs"](a, box, op)
+    got, _ = _run_env(ex, "bdbs", mono, a, box, {"EXSUM_BF_CUBIC": "1"})
+    gen, _ = _run_env(ex, "bdbs", mono, a, box, {"EXSUM_BF_CUBIC": "0"})
+    assert _bits_equal(got, want), (shape, box, mono)
+    assert _bits_equal(gen, want), (shape, box, mono)
+    if mono != "max-i64":
+        gotc, _ = _run_env(ex, "bdbsc", mono, a, box, {"EXSUM_BF_CUBIC": "1"})
+        if a.dtype.kind == "i":
+            assert _bits_equal(gotc, orc.ROUTES["bdbsc"](a, box, "add")), (shape, box, mono)
+        else:
+            ok, ratio, _ = compare("bdbsc", gotc, float64_oracle("bdbsc", a, box, orc), a, box, orc)
+            assert ok, (shape, box, mono, ratio)
