@@ -192,16 +192,43 @@ template <class F>
 int run_chain(const Shape& s, const PassPlan& p, int dtype, int op, const void* src,
               void* final_dst, void* other, const void* epi_total, cudaStream_t st,
               int* launches, bool live, PassExtra* ex0, F after_first) {
+  // steps: one pass, or two consecutive small strided axes as one outer pair
+  // (outer_pair.cu) when every buffer of the chain is 16-byte aligned
+  const size_t es = dtype_size(dtype);
+  const bool al = aligned16(src) && aligned16(final_dst) && (!other || aligned16(other));
+  int first[EXSUM_MAX_DIMS], len[EXSUM_MAX_DIMS], nsteps = 0;
+  for (int i = 0; i < p.count;) {
+    const int a = p.axes[i];
+    const bool pair = al && i + 1 < p.count && p.axes[i + 1] == a + 1 && a + 2 < s.d &&
+                      !(i == 0 && ex0) &&
+                      outer_pair_ok(dtype, op, s.ext[a], s.ext[a + 1], prod(s.ext, a + 2, s.d),
+                                    s.k[a], s.k[a + 1]);
+    first[nsteps] = i;
+    len[nsteps++] = pair ? 2 : 1;
+    i += pair ? 2 : 1;
+  }
   const void* cur = src;
-  for (int i = 0; i < p.count; ++i) {
-    const int remaining = p.count - 1 - i;
+  for (int j = 0; j < nsteps; ++j) {
+    const int remaining = nsteps - 1 - j;
     void* dst = (remaining % 2 == 0) ? final_dst : other;
+    const int i = first[j];
     if (live) {
-      int rc = one_pass(s, p.axes[i], dtype, op, cur, dst, i == p.count - 1 ? epi_total : nullptr,
-                        st, launches, i == 0 ? ex0 : nullptr);
-      if (rc) return rc;
+      const void* epi = j == nsteps - 1 ? epi_total : nullptr;
+      if (len[j] == 2) {
+        const int a = p.axes[i];
+        ProfScope ps("outer_pair", 2.0 * (double)s.N * es, st);
+        const int rc = launch_outer_pair(dtype, op, cur, dst, prod(s.ext, 0, a), s.ext[a],
+                                         s.ext[a + 1], prod(s.ext, a + 2, s.d), s.k[a], s.k[a + 1],
+                                         epi, st);
+        if (rc <= 0) return fail(EXSUM_ECUDA, "outer pass pair failed to launch");
+        *launches += rc;
+      } else {
+        int rc = one_pass(s, p.axes[i], dtype, op, cur, dst, epi, st, launches,
+                          i == 0 ? ex0 : nullptr);
+        if (rc) return rc;
+      }
     }
-    if (i == 0) {
+    if (j == 0) {
       int rc = after_first();
       if (rc) return rc;
     }

@@ -104,6 +104,13 @@ int block_fused_plan(int dtype, int d, const int64_t* ext, const int64_t* k, int
 int launch_block_fused(int dtype, int op, const void* in, void* out, int64_t N, const BlockSpec& bs,
                        const void* total, cudaStream_t s);
 
+// Two consecutive strided passes (axes a, a+1 of equal extent 16 or 28, one
+// window) in one HBM round trip over [outer, na, nb, inner] (outer_pair.cu)
+int outer_pair_ok(int dtype, int op, int64_t na, int64_t nb, int64_t inner, int64_t ka, int64_t kb);
+int launch_outer_pair(int dtype, int op, const void* in, void* out, int64_t outer, int64_t na,
+                      int64_t nb, int64_t inner, int64_t ka, int64_t kb, const void* total,
+                      cudaStream_t s);
+
 // L2-pipelined 3-D schedule (l2pipe.cu; opt-in EXSUM_L2PIPE=1): float32
 // [n0, n1, 1024] with box 16^3 in one persistent kernel -- mode 0 bdbs,
 // mode 1 the box-complement W passes + row round with tail T.
