@@ -5,13 +5,13 @@
 // non-contiguous axes a, a+1 of small extent (the dimension sweep's 28^5 and
 // 16^6: 28 x 28 and 16 x 16) the pair of passes only mixes elements of one
 // (a, a+1) plane per column of the remaining axes, so a CTA can take the whole
-// NA x NB plane for a strip of S columns (128 bytes: 32 float32 / 16 int64),
+// NA x NB plane for a strip of S = 16 columns (64 / 128 bytes),
 // run both passes in shared memory, and write the strip back once: 2 N s
 // bytes for the two passes instead of 4 N s.
 //
 // B200 mapping:
-//   * the strip's NA*NB rows of 128 bytes (one L2 line each; consecutive CTAs
-//     take consecutive strips, so the array streams) arrive as 16-byte cp.async
+//   * the strip's NA*NB rows of 64-128 bytes (consecutive CTAs take
+//     consecutive strips, so the array streams) arrive as 16-byte cp.async
 //     copies, the whole tile in flight; they leave as 16-byte streaming stores
 //     with the BDBSC complement epilogue;
 //   * shared layout [xa][xb][c] with c contiguous: a warp walks 32 lines that
@@ -63,11 +63,17 @@ __device__ __forceinline__ void op_line(At at) {
   }
 }
 
+// strip width: 16 columns (64 bytes of float32, 128 of int64 / float64).
+// Measured: float32 strips of 64 bytes beat 128 (C3d 0.044 -> 0.041 ms: a
+// 28 x 28 x 16 tile is 50 KB, 4 CTAs per SM instead of 2), 8-byte strips of
+// 64 bytes lost (0.059 -> 0.063 ms)
+constexpr int OP_S = 16;
+
 template <class T, class Op, int K, int NA, int NB>
 __global__ void __launch_bounds__(1024)
 k_outer_pair(const T* __restrict__ in, T* __restrict__ out, int64_t outer, int64_t inner,
              int pass_a, int pass_b, const typename AccOf<T>::type* __restrict__ total) {
-  constexpr int S = 128 / sizeof(T);  // strip columns
+  constexpr int S = OP_S;  // strip columns
   constexpr int VE = 16 / sizeof(T);
   constexpr int SV = S / VE;          // vectors per strip row
   constexpr int ROWS = NA * NB;
@@ -125,7 +131,7 @@ k_outer_pair(const T* __restrict__ in, T* __restrict__ out, int64_t outer, int64
 template <class T, class Op, int K, int NA, int NB>
 int go_outer(const T* in, T* out, int64_t outer, int64_t inner, int pass_a, int pass_b,
              const typename AccOf<T>::type* total, cudaStream_t s) {
-  constexpr int S = 128 / sizeof(T);
+  constexpr int S = OP_S;
   const size_t smem = (size_t)NA * NB * S * sizeof(T);
   // threads: the larger pass's lines in as few equal rounds as 1024 allow
   const int lines = (NA > NB ? NA : NB) * S;
@@ -175,7 +181,7 @@ int outer_pair_ok(int dtype, int op, int64_t na, int64_t nb, int64_t inner, int6
   if (!((dtype == F32 && op == ADD) || (dtype == F64 && op == ADD) || (dtype == I64 && op == ADD) ||
         (dtype == I64 && op == MAX)))
     return 0;
-  const int64_t S = 128 / (int64_t)dtype_size(dtype);
+  const int64_t S = OP_S;
   if (na != nb || !(na == 16 || na == 28) || inner % S != 0) return 0;
   const int64_t k = ka > 1 ? ka : kb;
   if (ka <= 1 || kb <= 1 || ka != kb) return 0;  // two real passes with one window

@@ -69,7 +69,7 @@ CASES = [
     ((28, 28, 28, 32), (4, 4, 4, 4)),
     ((16, 16, 64), (2, 2, 2)),
     ((28, 28, 32), (8, 8, 8)),           # float32 only (8-byte k = 8 takes the single passes)
-    ((28, 28, 20), (4, 4, 4)),           # inner not a strip multiple: single passes
+    ((28, 28, 20), (4, 4, 4)),           # inner not a multiple of the 16-column strip: single passes
 ]
 
 
