@@ -17,6 +17,10 @@ int fused_pair_ok(int dtype, int op, int64_t n2, int64_t k1, int64_t k2, int mod
   if (!env) return 0;
   if (dtype != F32 && dtype != F64 && dtype != I64) return 0;
   if (op == MAX && dtype != I64) return 0;
+  // rows longer than the widest template run as strips of it (ROW_WIN only)
+  const int64_t wmax = dtype == F32 ? 1024 : 512;
+  const bool strip = mode == ROW_WIN && n2 > wmax && n2 % wmax == 0 && n2 / wmax <= (1 << 20);
+  if (strip) n2 = wmax;
   if (n2 != 256 && n2 != 512 && n2 != 1024) return 0;
   if (n2 == 1024 && dtype != F32) return 0;
   const int C = (int)(n2 / 32);
@@ -27,7 +31,8 @@ int fused_pair_ok(int dtype, int op, int64_t n2, int64_t k1, int64_t k2, int mod
   const int VE = 16 / es;
   const int PSV = (C / VE + 1) | 1;
   const int64_t U = (16 / k1) * k1;
-  const size_t smem = ((size_t)2 * U * n2 + (size_t)U * 32 * PSV * VE) * es;
+  const int HV = strip ? (int)((k1 - 1 + VE - 1) / VE) : 0;
+  const size_t smem = ((size_t)2 * U * (n2 + HV * VE) + (size_t)U * (strip ? 33 : 32) * PSV * VE) * es;
   return smem <= 220 * 1024 ? 1 : 0;
 }
 

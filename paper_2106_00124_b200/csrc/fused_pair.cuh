@@ -73,15 +73,20 @@ __host__ __device__ constexpr int fp_chunk_stride(int CV, int MODE) {
   return fp_swizzled(CV, MODE) ? CV : ((CV + 1) | 1);
 }
 
-template <class T, class Op, int C, int K1, int MODE, int TV>
+template <class T, class Op, int C, int K1, int MODE, int TV, bool STRIP>
 // narrow rows ask for more resident CTAs: a register cap that raises the warps
 // per SM there (4-byte, 64-thread CTAs: 12, C3b 0.033 -> 0.030 ms; 8-byte,
 // 128 threads: 4, C2 0.066 -> 0.062 ms, except the max row op, which spills)
-__global__ void __launch_bounds__(32 * C / TV,
+// STRIP (ROW_WIN on rows longer than 32 C): the CTA takes a strip of 32 C
+// columns plus a right halo of K1 - 1 columns streamed by one extra warp, so
+// the row op's last block sees its neighbour block; the halo's outputs belong
+// to the next strip and are not stored
+__global__ void __launch_bounds__(32 * C / TV + (STRIP ? 32 : 0),
                                    (C <= 8 ? (sizeof(T) == 4 ? 12 : (MODE == ROW_EXCL ? 1 : 4)) : 1))
 k_fused_pair(const T* __restrict__ in, T* __restrict__ out, int64_t outer, int64_t n1,
              int64_t kx, int64_t seg_len, int64_t nseg,
-             const typename AccOf<T>::type* __restrict__ total, const T* __restrict__ Tail) {
+             const typename AccOf<T>::type* __restrict__ total, const T* __restrict__ Tail,
+             int64_t n2full, int64_t nstrips) {
   constexpr int VE = 16 / sizeof(T);  // 16-byte vector (stage layout, row op)
   constexpr int N2 = 32 * C;           // row length
   constexpr int NT = N2 / TV;          // threads: one TV-element column vector each
@@ -94,7 +99,9 @@ k_fused_pair(const T* __restrict__ in, T* __restrict__ out, int64_t outer, int64
   // 0.084 -> 0.090 ms); padded chunks (odd stride) otherwise
   constexpr bool SWZ = fp_swizzled(CV, MODE);
   constexpr int CH = fp_chunk_stride(CV, MODE) * VE;  // chunk stride (elements)
-  constexpr int ROWP = 32 * CH;                       // stage row length (elements)
+  constexpr int HV = STRIP ? (K1 - 1 + VE - 1) / VE : 0;  // halo vectors per row
+  constexpr int RAWP = N2 + HV * VE;                 // ring row pitch
+  constexpr int ROWP = (STRIP ? 33 : 32) * CH;       // stage row length (elements; chunk 32 = halo)
   // stage offset of element e of a row / of vector v of lane L's chunk
   auto eoff = [](int64_t e) -> int64_t {
     if constexpr (SWZ) return fp_swz<CV>((int)(e / VE)) * VE + (e % VE);
@@ -108,30 +115,44 @@ k_fused_pair(const T* __restrict__ in, T* __restrict__ out, int64_t outer, int64
   typedef Vec<T, VE> VT;  // row-op vectors
   typedef Vec<T, TV> CT;  // column vectors of the axis-(d-2) pass
   extern __shared__ __align__(16) unsigned char smem[];
-  T* raw = reinterpret_cast<T*>(smem);  // [2][U][N2]
-  T* wst = raw + 2 * U * N2;            // [U][ROWP]
+  T* raw = reinterpret_cast<T*>(smem);  // [2][U][RAWP]
+  T* wst = raw + 2 * U * RAWP;          // [U][ROWP]
   const int tid = threadIdx.x;
   const int lane = tid & 31;
   const int warp = tid >> 5;
-  const int col = tid * TV;
+  const bool halo_thr = STRIP && tid >= NT;   // the halo warp
+  const int hv = tid - NT;                    // its column vector
+  const bool colthr = !halo_thr || hv < HV;   // owns a column vector
+  const int col = halo_thr ? N2 + hv * TV : tid * TV;
   static_assert(TV == VE, "the stage swizzle assumes 16-byte column vectors");
-  const int pcol = SWZ ? fp_swz<CV>(tid) * VE : (col / C) * CH + (col % C);  // this thread's column vector in a stage row
+  static_assert(!STRIP || (!SWZ && MODE == ROW_WIN && HV * VE <= CH), "strip layout");
+  const int pcol = halo_thr ? 32 * CH + hv * VE
+                            : SWZ ? fp_swz<CV>(tid) * VE : (col / C) * CH + (col % C);  // this thread's column vector in a stage row
   const T ident = Op::template identity<T>();
   const T tot = total ? (T)(*total) : T(0);
   const bool epi = total != nullptr;
   const int64_t last_bs = (int64_t)K1 * ((n1 - 1) / K1);
-  const int64_t items = outer * nseg;
+  // row stride and strip count: compile-time without strips (the stride
+  // stays an immediate in the streaming loops)
+  const int64_t rs = STRIP ? n2full : (int64_t)N2;
+  const int64_t nst = STRIP ? nstrips : 1;
+  const int64_t items = outer * nseg * nst;
   const bool kvec = (kx % VE) == 0;
 
   for (int64_t item = blockIdx.x; item < items; item += gridDim.x) {
-    const int64_t o = item / nseg;
-    const int64_t seg = item % nseg;
+    // strips fastest: the CTAs in flight cover whole rows
+    const int64_t strip = STRIP ? item % nst : 0;
+    const int64_t os = STRIP ? item / nst : item;
+    const int64_t o = os / nseg;
+    const int64_t seg = os % nseg;
+    const bool last_strip = strip + 1 == nst;
+    const bool loads = colthr && !(halo_thr && last_strip);  // no halo past the row end
     const int64_t xs = seg * seg_len;  // multiple of U
     const int64_t xe = xs + seg_len < n1 ? xs + seg_len : n1;
     const int64_t u0 = xs / U;
     const int64_t u_end = (xe + U - 1) / U;
-    const T* src = in + o * n1 * N2 + col;
-    T* dst = out + o * n1 * N2 + col;
+    const T* src = in + o * n1 * rs + strip * N2 + col;
+    T* dst = out + o * n1 * rs + strip * N2 + col;
 
     // rows loaded for unit ui: the whole unit inside the segment; past the
     // segment only the first block's K1-1 rows (the stitch partner)
@@ -142,8 +163,9 @@ k_fused_pair(const T* __restrict__ in, T* __restrict__ out, int64_t outer, int64
     };
     auto issue = [&](int64_t ui) {
       const int rows = rows_of(ui);
-      T* d = raw + ((ui - u0) & 1) * (U * N2) + col;
-      for (int r = 0; r < rows; ++r) cp_async_n<TV * sizeof(T)>(d + r * N2, src + (ui * U + r) * N2);
+      T* d = raw + ((ui - u0) & 1) * (U * RAWP) + col;
+      if (loads)
+        for (int r = 0; r < rows; ++r) cp_async_n<TV * sizeof(T)>(d + r * RAWP, src + (ui * U + r) * rs);
       cp_async_commit();  // always commit: uniform group accounting
     };
 
@@ -154,7 +176,7 @@ k_fused_pair(const T* __restrict__ in, T* __restrict__ out, int64_t outer, int64
     int len = rows_of(u0);
 #pragma unroll
     for (int r = 0; r < U; ++r)
-      if (r < len) cur[r] = *reinterpret_cast<const CT*>(raw + col + r * N2);
+      if (r < len) cur[r] = *reinterpret_cast<const CT*>(raw + col + r * RAWP);
     issue(u0 + 2);
 
     for (int64_t u = u0; u < u_end; ++u) {
@@ -179,13 +201,13 @@ k_fused_pair(const T* __restrict__ in, T* __restrict__ out, int64_t outer, int64
       constexpr bool EARLY = true;
       constexpr int NX = EARLY ? U : K1;
       const int nlen_u = rows_of(u + 1);
-      const T* sn = raw + ((u + 1 - u0) & 1) * (U * N2) + col;
+      const T* sn = raw + ((u + 1 - u0) & 1) * (U * RAWP) + col;
       CT nxt[NX];
       if (nlen_u > 0) {
         cp_async_wait<1>();  // unit u+1 has landed (u+2 may still be in flight)
 #pragma unroll
         for (int r = 0; r < NX; ++r)
-          if (r < nlen_u) nxt[r] = *reinterpret_cast<const CT*>(sn + r * N2);
+          if (r < nlen_u) nxt[r] = *reinterpret_cast<const CT*>(sn + r * RAWP);
       }
       if constexpr (EARLY) issue(u + 3);  // refills the slot unit u+1 just vacated
 #pragma unroll
@@ -204,12 +226,12 @@ k_fused_pair(const T* __restrict__ in, T* __restrict__ out, int64_t outer, int64
           if (bs == last_bs) {  // last block of axis d-2: W = S
 #pragma unroll
             for (int r = 0; r < K1; ++r)
-              if (r < blen) *reinterpret_cast<CT*>(wst + (jb * K1 + r) * ROWP + pcol) = cur[jb * K1 + r];
+              if (r < blen && colthr) *reinterpret_cast<CT*>(wst + (jb * K1 + r) * ROWP + pcol) = cur[jb * K1 + r];
           } else {
             // stitch with the next block's left-nested prefix (raw)
             const int64_t nrows = n1 - bs - K1;
             const int nlen = (int)(nrows < K1 ? nrows : K1);
-            *reinterpret_cast<CT*>(wst + (jb * K1) * ROWP + pcol) = cur[jb * K1];
+            if (colthr) *reinterpret_cast<CT*>(wst + (jb * K1) * ROWP + pcol) = cur[jb * K1];
             const int nb0 = jb + 1 < G ? (jb + 1) * K1 : 0;  // in range for the dead branch
             CT P = jb + 1 < G ? cur[nb0] : nxt[0];
 #pragma unroll
@@ -223,7 +245,7 @@ k_fused_pair(const T* __restrict__ in, T* __restrict__ out, int64_t outer, int64
               CT w;
 #pragma unroll
               for (int j = 0; j < TV; ++j) w.v[j] = Op::apply(cur[jb * K1 + r].v[j], P.v[j]);
-              *reinterpret_cast<CT*>(wst + (jb * K1 + r) * ROWP + pcol) = w;
+              if (colthr) *reinterpret_cast<CT*>(wst + (jb * K1 + r) * ROWP + pcol) = w;
             }
           }
         }
@@ -243,7 +265,7 @@ k_fused_pair(const T* __restrict__ in, T* __restrict__ out, int64_t outer, int64
 #pragma unroll (MODE == ROW_EXCL ? 1 : RPW)
       for (int ri = 0; ri < RPW; ++ri) {
         const int rr = warp + ri * NW;
-        if (rr >= rows_u) break;
+        if (rr >= rows_u || (STRIP && warp >= NW)) break;
         T* wrow = wst + rr * ROWP;
         T* mine = wrow + lane * CH;  // padded layout: this lane's chunk
         // vector v of lane L's chunk (L = lane or lane + 1)
@@ -273,7 +295,7 @@ k_fused_pair(const T* __restrict__ in, T* __restrict__ out, int64_t outer, int64
           // exact in-block scans along the row (blocks of K2 inside the chunk)
           constexpr int NBV = (K2 + VE - 1) / VE;
           VT nbv[NBV];  // neighbour's first block, raw
-          if (lane < 31) {
+          if (lane < 31 || (STRIP && !last_strip)) {  // lane 31 of a strip: the halo chunk
 #pragma unroll
             for (int v = 0; v < NBV; ++v)
               nbv[v] = *reinterpret_cast<const VT*>(cvec(lane + 1, v));
@@ -282,7 +304,7 @@ k_fused_pair(const T* __restrict__ in, T* __restrict__ out, int64_t outer, int64
           for (int j = 0; j < M2; ++j) {
 #pragma unroll
             for (int r = K2 - 2; r >= 0; --r) a[j * K2 + r] = Op::apply(a[j * K2 + r], a[j * K2 + r + 1]);
-            const bool last = (lane == 31) && (j == M2 - 1);  // n2 % K2 == 0
+            const bool last = (lane == 31) && (j == M2 - 1) && (!STRIP || last_strip);  // n2 % K2 == 0
             if (!last) {
               if (j + 1 < M2) {
                 T Pr = a[(j + 1) * K2];
@@ -530,13 +552,14 @@ k_fused_pair(const T* __restrict__ in, T* __restrict__ out, int64_t outer, int64
         __syncwarp();
       }
       __syncthreads();
-      for (int r = 0; r < rows_u; ++r)
-        st_stream<T, TV>(dst + (us + r) * N2, *reinterpret_cast<const CT*>(wst + r * ROWP + pcol));
+      if (!halo_thr)
+        for (int r = 0; r < rows_u; ++r)
+          st_stream<T, TV>(dst + (us + r) * rs, *reinterpret_cast<const CT*>(wst + r * ROWP + pcol));
       if constexpr (!EARLY) {
         if (u + 1 < u_end) {
 #pragma unroll
           for (int r = 0; r < U; ++r)
-            if (r < nlen_u) cur[r] = *reinterpret_cast<const CT*>(sn + r * N2);
+            if (r < nlen_u) cur[r] = *reinterpret_cast<const CT*>(sn + r * RAWP);
         }
         issue(u + 3);  // refills the slot unit u+1 just vacated
       }
@@ -552,45 +575,50 @@ constexpr int pick_tv() {
                                                  : (32 * C) / 256 >= 1 ? (32 * C) / 256 : 1;
 }
 
-template <class T, class Op, int C, int K1, int MODE>
+template <class T, class Op, int C, int K1, int MODE, bool STRIP>
 int go_pair(const T* in, T* out, int64_t outer, int64_t n1, int64_t kx,
-            const typename AccOf<T>::type* total, const T* Tail, cudaStream_t s) {
+            const typename AccOf<T>::type* total, const T* Tail, int64_t n2full, cudaStream_t s) {
   constexpr int VE = 16 / sizeof(T);
   constexpr int TV = VE;  // 16-byte column vectors measured best (8-byte: -30% at C4)
   constexpr int N2 = 32 * C;
   constexpr int NT = N2 / TV;
   constexpr int CV = C / VE;
-  constexpr int ROWP = 32 * fp_chunk_stride(CV, MODE) * VE;
+  constexpr int HV = STRIP ? (K1 - 1 + VE - 1) / VE : 0;
+  constexpr int ROWP = (STRIP ? 33 : 32) * fp_chunk_stride(CV, MODE) * VE;
   constexpr int U = fp_unit_rows(C, K1);
-  const size_t smem = ((size_t)2 * U * N2 + (size_t)U * ROWP) * sizeof(T);
+  constexpr int NTA = NT + (STRIP ? 32 : 0);
+  const int64_t nstrips = STRIP ? n2full / N2 : 1;
+  const size_t smem = ((size_t)2 * U * (N2 + HV * VE) + (size_t)U * ROWP) * sizeof(T);
   if (smem > 220 * 1024) return -1;
   int per_sm = (int)((228 * 1024) / (smem + 1024));
-  if (per_sm > 2048 / NT) per_sm = 2048 / NT;
+  if (per_sm > 2048 / NTA) per_sm = 2048 / NTA;
   if (per_sm < 1) per_sm = 1;
   const int64_t nunits = (n1 + U - 1) / U;
   // segments per outer index (exsum_launch.h: wave rounding vs halo + fill)
-  int64_t nseg = pick_segments(outer, nunits, per_sm);
+  int64_t nseg = pick_segments(outer * nstrips, nunits, per_sm);
   const int64_t seg_len = U * ((nunits + nseg - 1) / nseg);
   nseg = (n1 + seg_len - 1) / seg_len;
-  const int64_t items = outer * nseg;
+  const int64_t items = outer * nseg * nstrips;
   int64_t grid = items;
   const int64_t cap = (int64_t)num_sms() * per_sm * 4;
   if (grid > cap) grid = cap;
-  ensure_smem((const void*)k_fused_pair<T, Op, C, K1, MODE, TV>, smem);
-  k_fused_pair<T, Op, C, K1, MODE, TV><<<(unsigned)grid, NT, smem, s>>>(in, out, outer, n1, kx,
-                                                                       seg_len, nseg, total, Tail);
+  ensure_smem((const void*)k_fused_pair<T, Op, C, K1, MODE, TV, STRIP>, smem);
+  k_fused_pair<T, Op, C, K1, MODE, TV, STRIP><<<(unsigned)grid, NTA, smem, s>>>(
+      in, out, outer, n1, kx, seg_len, nseg, total, Tail, STRIP ? n2full : (int64_t)N2, nstrips);
   return 1;
 }
 
-template <class T, class Op, int C, int MODE>
+template <class T, class Op, int C, int MODE, bool STRIP = false>
 int pick_k1(const T* in, T* out, int64_t outer, int64_t n1, int64_t k1, int64_t kx,
-            const typename AccOf<T>::type* total, const T* Tail, cudaStream_t s) {
+            const typename AccOf<T>::type* total, const T* Tail, cudaStream_t s,
+            int64_t n2full = 0) {
   switch (k1) {
-    case 2: return go_pair<T, Op, C, 2, MODE>(in, out, outer, n1, kx, total, Tail, s);
-    case 4: return go_pair<T, Op, C, 4, MODE>(in, out, outer, n1, kx, total, Tail, s);
-    case 8: return go_pair<T, Op, C, 8, MODE>(in, out, outer, n1, kx, total, Tail, s);
+    case 2: return go_pair<T, Op, C, 2, MODE, STRIP>(in, out, outer, n1, kx, total, Tail, n2full, s);
+    case 4: return go_pair<T, Op, C, 4, MODE, STRIP>(in, out, outer, n1, kx, total, Tail, n2full, s);
+    case 8: return go_pair<T, Op, C, 8, MODE, STRIP>(in, out, outer, n1, kx, total, Tail, n2full, s);
     case 16:
-      if constexpr (C >= 16) return go_pair<T, Op, C, 16, MODE>(in, out, outer, n1, kx, total, Tail, s);
+      if constexpr (C >= 16)
+        return go_pair<T, Op, C, 16, MODE, STRIP>(in, out, outer, n1, kx, total, Tail, n2full, s);
       return -1;
   }
   return -1;
@@ -601,6 +629,10 @@ int go_fused(const T* in, T* out, int64_t outer, int64_t n1, int64_t n2, int64_t
              int mode, const typename AccOf<T>::type* total, const T* Tail, cudaStream_t s) {
   if (((uintptr_t)in % 16) || ((uintptr_t)out % 16)) return -1;
   if (mode == ROW_WIN) {
+    // rows longer than the widest row template: strips of it with a halo
+    constexpr int CW = sizeof(T) == 4 ? 32 : 16;
+    if (n2 > 32 * CW && n2 % (32 * CW) == 0)
+      return pick_k1<T, Op, CW, ROW_WIN, true>(in, out, outer, n1, k1, 0, total, nullptr, s, n2);
     switch (n2) {
       case 256: return pick_k1<T, Op, 8, ROW_WIN>(in, out, outer, n1, k1, 0, total, nullptr, s);
       case 512: return pick_k1<T, Op, 16, ROW_WIN>(in, out, outer, n1, k1, 0, total, nullptr, s);

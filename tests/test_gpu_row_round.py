@@ -94,3 +94,35 @@ def test_row_round_extreme_values(ex, mono):
     else:
         ok, ratio, rel = compare("box-complement", got, want, a, box, orc)
         assert ok, (ratio, rel)
+
+
+# ROW_WIN on rows longer than the widest row template (1024 float32 / 512
+# 8-byte): strips of it with a halo warp (the C3a 4096^2 shape of the sweep)
+STRIP_CASES = [
+    ((4096, 4096), (4, 4), "add-f32"),
+    ((4096, 4096), (4, 4), "max-i64"),
+    ((37, 2048), (2, 2), "add-f32"),
+    ((37, 2048), (8, 8), "add-f32"),
+    ((21, 3072), (16, 16), "add-f32"),
+    ((3, 19, 1024), (1, 4, 4), "add-i64"),
+    ((19, 1536), (16, 16), "add-f64"),
+    ((19, 1536), (2, 2), "max-i64"),
+    ((2, 40, 4096), (2, 8, 8), "add-f64"),
+]
+
+
+@pytest.mark.parametrize("shape,box,mono", STRIP_CASES, ids=lambda v: str(v))
+def test_row_strips(ex, shape, box, mono):
+    import torch
+
+    a = _data(mono, shape, seed=sum(shape) + sum(box))
+    op = "max" if mono.startswith("max") else "add"
+    t = ex.Tensor(ex.Float32AddOps() if mono == "add-f32" else ex.resolve_monoid(mono),
+                  torch.from_numpy(a).cuda())
+    got = ex.bdbs_included(t, box).data.cpu().numpy()
+    want = orc.bdbs_included(a, box, op)
+    assert np.array_equal(got.view(np.uint8), want.view(np.uint8)), (shape, box, mono)
+    if op == "add":
+        gotc = ex.bdbs_excluded(t, box).data.cpu().numpy()
+        ok, ratio, rel = compare("bdbsc", gotc, orc.bdbs_excluded(a.astype(np.float64) if a.dtype.kind == "f" else a, box, "add"), a, box, orc)
+        assert ok, (shape, box, mono, ratio)
