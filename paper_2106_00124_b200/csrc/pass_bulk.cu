@@ -16,16 +16,25 @@
 // are O(1) in k; the ring keeps R-1 blocks of loads in flight per warp.
 #include <stdlib.h>
 
+#include <type_traits>
+
 #include "exsum_common.cuh"
 #include "exsum_launch.h"
 
 namespace exsum {
 
-template <class T, class Op>
+template <class T, class Op, bool TOT>
 __global__ void __launch_bounds__(32)
 k_strided_bulk(const T* __restrict__ in, T* __restrict__ out, int64_t outer, int64_t n,
                int64_t inner, int k, int64_t seg_len, int64_t nseg, int R,
-               const typename AccOf<T>::type* __restrict__ total) {
+               const typename AccOf<T>::type* __restrict__ total,
+               typename AccOf<T>::type* __restrict__ tpart) {
+  // tpart (BDBSC, excluded.py:72-75): this CTA's fold of the raw input rows it
+  // owns (the in-block suffix loops read each own row once), for
+  // launch_total_final -- the total rides on this pass instead of a separate
+  // read of the array
+  typedef typename AccOf<T>::type Acc;
+  Acc tacc = Acc(0);
   extern __shared__ __align__(128) unsigned char smem[];
   uint64_t* bar = reinterpret_cast<uint64_t*>(smem);  // R <= 15 barriers
   T* stg = reinterpret_cast<T*>(smem + 128);
@@ -86,9 +95,12 @@ k_strided_bulk(const T* __restrict__ in, T* __restrict__ out, int64_t outer, int
     int len = rows_of(b0);
     {  // in-block suffix of the first block, in place (right nested)
       T v = cur[(len - 1) * 32 + lane];
+      if constexpr (TOT) tacc = OpAdd::apply<Acc>(tacc, (Acc)v);
 #pragma unroll 8
       for (int r = len - 2; r >= 0; --r) {
-        v = Op::apply(cur[r * 32 + lane], v);
+        const T a = cur[r * 32 + lane];
+        if constexpr (TOT) tacc = OpAdd::apply<Acc>(tacc, (Acc)a);
+        v = Op::apply(a, v);
         cur[r * 32 + lane] = v;
       }
     }
@@ -123,9 +135,12 @@ k_strided_bulk(const T* __restrict__ in, T* __restrict__ out, int64_t outer, int
         cur = nxt;
         len = nlen;
         T v = cur[(len - 1) * 32 + lane];
+        if constexpr (TOT) tacc = OpAdd::apply<Acc>(tacc, (Acc)v);
 #pragma unroll 8
         for (int r = len - 2; r >= 0; --r) {
-          v = Op::apply(cur[r * 32 + lane], v);
+          const T a = cur[r * 32 + lane];
+          if constexpr (TOT) tacc = OpAdd::apply<Acc>(tacc, (Acc)a);
+          v = Op::apply(a, v);
           cur[r * 32 + lane] = v;
         }
       }
@@ -133,13 +148,18 @@ k_strided_bulk(const T* __restrict__ in, T* __restrict__ out, int64_t outer, int
     ncons += (uint32_t)nblk;
     __syncwarp();
   }
+  if constexpr (TOT) {
+#pragma unroll
+    for (int d = 16; d >= 1; d >>= 1) tacc = OpAdd::apply<Acc>(tacc, __shfl_xor_sync(0xffffffffu, tacc, d));
+    if (lane == 0) tpart[blockIdx.x] = tacc;
+  }
 }
 
 namespace {
 
 template <class T, class Op>
 int go_bulk(const T* in, T* out, int64_t outer, int64_t n, int64_t inner, int64_t k,
-            const typename AccOf<T>::type* total, cudaStream_t s) {
+            const typename AccOf<T>::type* total, cudaStream_t s, PassExtra* ex) {
   const size_t stage = (size_t)k * 32 * sizeof(T);
   // two stages (the block being stitched + the next block in flight): more
   // resident warps beat deeper per-warp prefetch (C5 f64: k=32 0.83 -> 0.71 ms,
@@ -165,10 +185,23 @@ int go_bulk(const T* in, T* out, int64_t outer, int64_t n, int64_t inner, int64_
   int64_t grid = items;
   const int64_t cap = (int64_t)num_sms() * 32;
   if (grid > cap) grid = cap;
-  if (smem > 48 * 1024)
-    ensure_smem((const void*)k_strided_bulk<T, Op>, smem);
-  k_strided_bulk<T, Op><<<(unsigned)grid, 32, smem, s>>>(in, out, outer, n, inner, (int)k,
-                                                         seg_len, nseg, R, total);
+  typedef typename AccOf<T>::type Acc;
+  Acc* tpart = nullptr;
+  if (ex && ex->kind == 2 && std::is_same<Op, OpAdd>::value && grid <= ex->cap) {
+    tpart = (Acc*)ex->buf;
+    ex->done = 1;
+    ex->ppr = grid;
+  }
+  if (ex) ex->n_out_done = 1;
+  if (tpart) {
+    if (smem > 48 * 1024) ensure_smem((const void*)k_strided_bulk<T, Op, true>, smem);
+    k_strided_bulk<T, Op, true><<<(unsigned)grid, 32, smem, s>>>(in, out, outer, n, inner, (int)k,
+                                                                 seg_len, nseg, R, total, tpart);
+  } else {
+    if (smem > 48 * 1024) ensure_smem((const void*)k_strided_bulk<T, Op, false>, smem);
+    k_strided_bulk<T, Op, false><<<(unsigned)grid, 32, smem, s>>>(in, out, outer, n, inner, (int)k,
+                                                                  seg_len, nseg, R, total, nullptr);
+  }
   return 1;
 }
 
@@ -176,16 +209,16 @@ int go_bulk(const T* in, T* out, int64_t outer, int64_t n, int64_t inner, int64_
 
 // Eligible when strips of 32 columns tile `inner` and rows are 16-byte aligned.
 int launch_strided_bulk(int dtype, int op, const void* in, void* out, int64_t outer, int64_t n,
-                        int64_t inner, int64_t k, const void* total, cudaStream_t s) {
+                        int64_t inner, int64_t k, const void* total, cudaStream_t s, PassExtra* ex) {
   if (inner % 32 != 0 || ((uintptr_t)in % 16) != 0 || ((uintptr_t)out % 16) != 0) return -1;
   if (dtype == F32 && op == ADD)
-    return go_bulk<float, OpAdd>((const float*)in, (float*)out, outer, n, inner, k, (const double*)total, s);
+    return go_bulk<float, OpAdd>((const float*)in, (float*)out, outer, n, inner, k, (const double*)total, s, ex);
   if (dtype == F64 && op == ADD)
-    return go_bulk<double, OpAdd>((const double*)in, (double*)out, outer, n, inner, k, (const double*)total, s);
+    return go_bulk<double, OpAdd>((const double*)in, (double*)out, outer, n, inner, k, (const double*)total, s, ex);
   if (dtype == I64 && op == ADD)
-    return go_bulk<i64, OpAdd>((const i64*)in, (i64*)out, outer, n, inner, k, (const i64*)total, s);
+    return go_bulk<i64, OpAdd>((const i64*)in, (i64*)out, outer, n, inner, k, (const i64*)total, s, ex);
   if (dtype == I64 && op == MAX)
-    return go_bulk<i64, OpMax>((const i64*)in, (i64*)out, outer, n, inner, k, nullptr, s);
+    return go_bulk<i64, OpMax>((const i64*)in, (i64*)out, outer, n, inner, k, nullptr, s, ex);
   return -2;
 }
 

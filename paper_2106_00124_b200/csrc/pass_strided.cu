@@ -448,7 +448,8 @@ int launch_rows_pass(int dtype, int op, const void* in, void* out, int64_t rows,
                      int64_t k, const void* total, cudaStream_t s);
 
 int launch_strided_bulk(int dtype, int op, const void* in, void* out, int64_t outer, int64_t n,
-                        int64_t inner, int64_t k, const void* total, cudaStream_t s);
+                        int64_t inner, int64_t k, const void* total, cudaStream_t s,
+                        PassExtra* ex);
 int launch_axis_stream_f32(const void*, void*, int64_t, int64_t, int64_t, int64_t, const void*,
                            cudaStream_t, PassExtra*);
 int launch_axis_stream_f64(const void*, void*, int64_t, int64_t, int64_t, int64_t, const void*,
@@ -511,7 +512,8 @@ int launch_pass(int dtype, int op, const void* in, void* out, int64_t outer, int
     if (rc >= 0) return rc;
   }
   if (mode == 2 || (mode == 0 && big)) {
-    const int rc = launch_strided_bulk(dtype, op, in, out, outer, n, inner, k, total, s);
+    const int rc = launch_strided_bulk(dtype, op, in, out, outer, n, inner, k, total, s,
+                                       ex && ex->kind == 2 ? ex : nullptr);
     if (rc >= 0) return rc;
   }
   if (dtype == F32 && op == ADD)
