@@ -32,6 +32,9 @@
 #include <cuda_runtime.h>
 
 #include <stdio.h>
+#include <string.h>
+
+extern char** environ;
 
 #include <mutex>
 #include <string>
@@ -747,6 +750,164 @@ int run_device(int route, const void* in, void* out, int dtype, int op, int64_t 
 }
 
 
+// ------------------------------------------------ CUDA-graph replay --
+// A device call repeated with the same arguments (route, shape, box, the
+// same in / out / workspace pointers -- a training or serving loop) is
+// captured once into a CUDA graph on a private stream and replayed with one
+// cudaGraphLaunch on the caller's stream: no per-call planning on the host
+// and no host launch gaps between the route's short kernels (C2: 6 launches,
+// 3-10 us each besides the two full passes).  First sighting of a key runs
+// directly; the second captures; later ones replay.  Anything the capture
+// cannot take (an error, the profiler on, EXSUM_GRAPH=0) runs directly.
+namespace {
+struct GraphEntry {
+  int route = 0, dtype = 0, op = 0, d = 0, dev = -1;
+  int64_t modulus = 0;
+  int64_t ext[EXSUM_MAX_DIMS] = {}, box[EXSUM_MAX_DIMS] = {};
+  const void* in = nullptr;
+  void* out = nullptr;
+  void* ws = nullptr;
+  size_t ws_bytes = 0;
+  uint64_t envh = 0;  // the EXSUM_* knobs the plan read
+  int seen = 0;
+  bool bad = false;
+  cudaGraphExec_t exec = nullptr;
+  int launches = 0;
+  uint64_t used = 0;
+};
+struct GraphCache {
+  std::mutex mu;
+  std::vector<GraphEntry> e;
+  std::vector<std::pair<int, cudaStream_t>> cap;  // capture stream per device
+  uint64_t tick = 0;
+};
+GraphCache& graph_cache() {
+  static GraphCache c;
+  return c;
+}
+bool graphs_on() {
+  static int on = -1;
+  if (on < 0) {
+    const char* v = getenv("EXSUM_GRAPH");
+    on = (v && v[0] == '0') ? 0 : 1;
+  }
+  return on == 1;
+}
+constexpr size_t kGraphCap = 32;
+// hash of the EXSUM_* environment: the planners read several knobs per call,
+// so a graph is only replayed under the settings it was captured with
+uint64_t exsum_env_hash() {
+  uint64_t h = 1469598103934665603ull;
+  for (char** e = environ; e && *e; ++e) {
+    if (strncmp(*e, "EXSUM_", 6) != 0) continue;
+    for (const char* p = *e; *p; ++p) h = (h ^ (unsigned char)*p) * 1099511628211ull;
+    h = (h ^ 0xff) * 1099511628211ull;
+  }
+  return h;
+}
+}  // namespace
+
+int run_device_graph(int route, const void* in, void* out, int dtype, int op, int64_t modulus,
+                     int d, const int64_t* ext, const int64_t* box, void* ws, size_t ws_bytes,
+                     void* stream) {
+  if (!graphs_on() || g_prof.on || d < 1 || d > EXSUM_MAX_DIMS || !ext || !box)
+    return run_device(route, in, out, dtype, op, modulus, d, ext, box, ws, ws_bytes, stream);
+  int dev = 0;
+  if (cudaGetDevice(&dev) != cudaSuccess) return cuda_check("cudaGetDevice");
+  const uint64_t envh = exsum_env_hash();
+  GraphCache& c = graph_cache();
+  std::unique_lock<std::mutex> lock(c.mu);
+  GraphEntry* hit = nullptr;
+  for (auto& g : c.e) {
+    if (g.route != route || g.dtype != dtype || g.op != op || g.d != d || g.dev != dev ||
+        g.modulus != modulus || g.in != in || g.out != out || g.ws != ws || g.ws_bytes != ws_bytes ||
+        g.envh != envh)
+      continue;
+    bool same = true;
+    for (int i = 0; i < d; ++i) same = same && g.ext[i] == ext[i] && g.box[i] == box[i];
+    if (same) {
+      hit = &g;
+      break;
+    }
+  }
+  if (!hit) {
+    if (c.e.size() >= kGraphCap) {  // evict the least recently used
+      size_t lru = 0;
+      for (size_t i = 1; i < c.e.size(); ++i)
+        if (c.e[i].used < c.e[lru].used) lru = i;
+      if (c.e[lru].exec) cudaGraphExecDestroy(c.e[lru].exec);
+      c.e.erase(c.e.begin() + (long)lru);
+    }
+    GraphEntry g;
+    g.route = route, g.dtype = dtype, g.op = op, g.d = d, g.dev = dev, g.modulus = modulus;
+    for (int i = 0; i < d; ++i) g.ext[i] = ext[i], g.box[i] = box[i];
+    g.in = in, g.out = out, g.ws = ws, g.ws_bytes = ws_bytes;
+    g.envh = envh;
+    g.seen = 1;
+    g.used = ++c.tick;
+    c.e.push_back(g);
+    lock.unlock();
+    return run_device(route, in, out, dtype, op, modulus, d, ext, box, ws, ws_bytes, stream);
+  }
+  hit->used = ++c.tick;
+  if (hit->bad) {
+    lock.unlock();
+    return run_device(route, in, out, dtype, op, modulus, d, ext, box, ws, ws_bytes, stream);
+  }
+  if (!hit->exec) {
+    // second sighting: capture on this device's private stream
+    cudaStream_t cs = nullptr;
+    for (auto& p : c.cap)
+      if (p.first == dev) cs = p.second;
+    if (!cs) {
+      if (cudaStreamCreateWithFlags(&cs, cudaStreamNonBlocking) != cudaSuccess) {
+        cudaGetLastError();
+        hit->bad = true;
+        lock.unlock();
+        return run_device(route, in, out, dtype, op, modulus, d, ext, box, ws, ws_bytes, stream);
+      }
+      c.cap.push_back({dev, cs});
+    }
+    cudaGraph_t graph = nullptr;
+    int rc = EXSUM_OK;
+    if (cudaStreamBeginCapture(cs, cudaStreamCaptureModeThreadLocal) == cudaSuccess) {
+      rc = run_device(route, in, out, dtype, op, modulus, d, ext, box, ws, ws_bytes, (void*)cs);
+      const cudaError_t ce = cudaStreamEndCapture(cs, &graph);
+      if (ce != cudaSuccess) rc = rc ? rc : EXSUM_ECUDA;
+    } else {
+      rc = EXSUM_ECUDA;
+    }
+    cudaGraphExec_t exec = nullptr;
+    if (rc == EXSUM_OK && graph && cudaGraphInstantiate(&exec, graph, 0) != cudaSuccess) exec = nullptr;
+    if (graph) cudaGraphDestroy(graph);
+    if (rc != EXSUM_OK || !exec) {
+      cudaGetLastError();  // clear a capture error; the direct call reports its own
+      hit->bad = true;
+      lock.unlock();
+      return run_device(route, in, out, dtype, op, modulus, d, ext, box, ws, ws_bytes, stream);
+    }
+    hit->exec = exec;
+    hit->launches = g_last_launches;
+    g_total_launches -= g_last_launches;  // captured, not launched
+  }
+  const cudaGraphExec_t exec = hit->exec;
+  const int launches = hit->launches;
+  lock.unlock();
+  g_err.clear();
+  if (cudaGraphLaunch(exec, (cudaStream_t)stream) != cudaSuccess) return cuda_check("cudaGraphLaunch");
+  g_last_launches = launches;
+  g_total_launches += launches;
+  return EXSUM_OK;
+}
+
+void release_graphs() {
+  GraphCache& c = graph_cache();
+  std::lock_guard<std::mutex> lock(c.mu);
+  for (auto& g : c.e)
+    if (g.exec) cudaGraphExecDestroy(g.exec);
+  c.e.clear();
+}
+
 // ----------------------------------------------------- shard stages (8e) --
 // Axis-0 sharding (paper_2106_00124_b200/sharded.py): a rank owns planes
 // [x_s, x_e) of axis 0 and receives the next rank's first k0-1 planes as a
@@ -967,23 +1128,23 @@ int exsum_workspace_bytes(int route, int dtype, int op, int d, const int64_t* ex
 
 int exsum_route(int route, const void* in, void* out, int dtype, int op, int64_t modulus, int d,
                 const int64_t* ext, const int64_t* box, void* ws, size_t ws_bytes, void* stream) {
-  return run_device(route, in, out, dtype, op, modulus, d, ext, box, ws, ws_bytes, stream);
+  return run_device_graph(route, in, out, dtype, op, modulus, d, ext, box, ws, ws_bytes, stream);
 }
 
 int exsum_bdbs_included(const void* in, void* out, int dtype, int op, int d, const int64_t* ext,
                         const int64_t* box, void* ws, size_t ws_bytes, void* stream) {
-  return run_device(EXSUM_ROUTE_BDBS, in, out, dtype, op, 0, d, ext, box, ws, ws_bytes, stream);
+  return run_device_graph(EXSUM_ROUTE_BDBS, in, out, dtype, op, 0, d, ext, box, ws, ws_bytes, stream);
 }
 
 int exsum_bdbsc_excluded(const void* in, void* out, int dtype, int op, int d, const int64_t* ext,
                          const int64_t* box, void* ws, size_t ws_bytes, void* stream) {
-  return run_device(EXSUM_ROUTE_BDBSC, in, out, dtype, op, 0, d, ext, box, ws, ws_bytes, stream);
+  return run_device_graph(EXSUM_ROUTE_BDBSC, in, out, dtype, op, 0, d, ext, box, ws, ws_bytes, stream);
 }
 
 int exsum_box_complement_excluded(const void* in, void* out, int dtype, int op, int d,
                                   const int64_t* ext, const int64_t* box, void* ws,
                                   size_t ws_bytes, void* stream) {
-  return run_device(EXSUM_ROUTE_BOX_COMPLEMENT, in, out, dtype, op, 0, d, ext, box, ws, ws_bytes,
+  return run_device_graph(EXSUM_ROUTE_BOX_COMPLEMENT, in, out, dtype, op, 0, d, ext, box, ws, ws_bytes,
                     stream);
 }
 
@@ -1420,6 +1581,7 @@ int exsum_box_complement_finish(const void* in, void* out, int dtype, int op, in
 }
 
 int exsum_release_cache(void) {
+  release_graphs();
   {
     BatchCache& b = batch_cache();
     std::lock_guard<std::mutex> lock(b.mu);
