@@ -205,9 +205,15 @@ int num_sms();
 // more than a short halo (C5 f64: 512 single-line items on 148 SMs were 3.46
 // waves).  Smaller CTAs keep ~3 waves of items so several stay resident per SM.
 inline int64_t pick_segments(int64_t lines, int64_t nunits, int per_sm) {
-  int64_t max_seg = nunits / 4;
-  if (max_seg < 1) max_seg = 1;
   const int64_t slots = (int64_t)num_sms() * per_sm;
+  // segments of >= 4 units bound the halo re-reads; an array too small to
+  // fill the machine that way (the box-complement tail levels: one 1024-row
+  // line) takes segments down to one unit
+#ifndef EXSUM_SMALL_SEG
+#define EXSUM_SMALL_SEG 1
+#endif
+  int64_t max_seg = (EXSUM_SMALL_SEG && lines * (nunits / 4) < slots) ? nunits : nunits / 4;
+  if (max_seg < 1) max_seg = 1;
   if (per_sm > 1) {
     int64_t nseg = (slots * 3 + lines - 1) / lines;
     if (nseg > max_seg) nseg = max_seg;
