@@ -810,8 +810,14 @@ uint64_t exsum_env_hash() {
 int run_device_graph(int route, const void* in, void* out, int dtype, int op, int64_t modulus,
                      int d, const int64_t* ext, const int64_t* box, void* ws, size_t ws_bytes,
                      void* stream) {
-  if (!graphs_on() || g_prof.on || d < 1 || d > EXSUM_MAX_DIMS || !ext || !box)
+  if (!graphs_on() || g_prof.on || d < 1 || d > EXSUM_MAX_DIMS || !ext || !box || !in || !out ||
+      in == out)
     return run_device(route, in, out, dtype, op, modulus, d, ext, box, ws, ws_bytes, stream);
+  {  // argument errors report exactly as the direct path (before any CUDA call)
+    Shape sh;
+    if (validate(route, dtype, op, modulus, d, ext, box, &sh) != EXSUM_OK)
+      return run_device(route, in, out, dtype, op, modulus, d, ext, box, ws, ws_bytes, stream);
+  }
   int dev = 0;
   if (cudaGetDevice(&dev) != cudaSuccess) return cuda_check("cudaGetDevice");
   const uint64_t envh = exsum_env_hash();
