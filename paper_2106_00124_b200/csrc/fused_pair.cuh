@@ -82,7 +82,8 @@ template <class T, class Op, int C, int K1, int MODE, int TV, bool STRIP>
 // the row op's last block sees its neighbour block; the halo's outputs belong
 // to the next strip and are not stored
 __global__ void __launch_bounds__(32 * C / TV + (STRIP ? 32 : 0),
-                                   (C <= 8 ? (sizeof(T) == 4 ? 12 : (MODE == ROW_EXCL ? 1 : 4)) : 1))
+                                   (C <= 8 ? (sizeof(T) == 4 ? (MODE == ROW_EXCL_BLK && K1 >= 8 ? 8 : 12)
+                                                  : (MODE == ROW_EXCL ? 1 : 4)) : 1))
 k_fused_pair(const T* __restrict__ in, T* __restrict__ out, int64_t outer, int64_t n1,
              int64_t kx, int64_t seg_len, int64_t nseg,
              const typename AccOf<T>::type* __restrict__ total, const T* __restrict__ Tail,
@@ -641,10 +642,13 @@ int go_fused(const T* in, T* out, int64_t outer, int64_t n1, int64_t n2, int64_t
         return -1;
     }
   } else {
-    // + with a cubic box: row total minus the exact windowed row op (8-byte
-    // elements for k <= 4 or 256-wide rows: larger windows on wider rows spill;
-    // C2 int64 box-complement fused pass 0.084 -> 0.060 ms)
-    if constexpr (std::is_same<Op, OpAdd>::value) {
+    // integer + with a cubic box: row total minus the exact windowed row op
+    // (two's-complement wrap makes the inverse exact; 8-byte elements for
+    // k <= 4 or 256-wide rows: larger windows on wider rows spill; C2 int64
+    // box-complement fused pass 0.084 -> 0.060 ms).  Floats never take it:
+    // box-complement is the strong route, no subtraction anywhere
+    // (excluded.py:130) -- they take ROW_EXCL_BLK below.
+    if constexpr (std::is_same<Op, OpAdd>::value && std::is_integral<T>::value) {
       if (k2 == k1 && (sizeof(T) == 4 || k1 <= 4 || n2 == 256)) {
         switch (n2) {
           case 256: return pick_k1<T, Op, 8, ROW_EXCL_ADD>(in, out, outer, n1, k1, k2, nullptr, Tail, s);

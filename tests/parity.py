@@ -10,9 +10,13 @@ Exactness contract (north star):
     feeds x, and tau = D * u with u the unit roundoff of the data type and D
     a bound on the number of roundings on any path to x:
       - BDBSC: S(x) = sum(|A|) (the total dominates), D = sum_i(2 k_i) + 8;
-      - box-complement: S(x) = box_complement(|A|)(x) + included(|A|)(x)
-        (all terms are partial sums of |A| over subsets of the array), and
-        D = sum_i(n_i + 2 k_i) + 16 (full-axis scans are the longest chains).
+      - box-complement: S(x) = box_complement(|A|)(x), the same route applied
+        to |A|.  The route is strong: every term feeding x is a
+        partial sum of |A| over a subset of x's complement (no subtraction
+        anywhere, excluded.py:130), so an inverse-free evaluation's error is
+        bounded by D * u * S(x) with D = sum_i(n_i + 2 k_i) + 16 (full-axis
+        scans are the longest chains).  A weak evaluation (row total minus
+        window) would not meet it where x's box holds large mass.
       - sat / satc: every table entry is a prefix sum bounded by
         sum(|A|) and the query folds 2^d of them, so S(x) = 2^d * sum(|A|)
         (+ sum(|A|) for satc's total) and D = sum_i(n_i) + 2^d + 8.  Where the
@@ -52,7 +56,7 @@ def float_tolerance(route, a, k, oracle_mod):
     elif route in ("sat", "satc"):
         S = np.full(ext, (2 ** len(ext) + (route == "satc")) * a64.sum())
     elif route == "box-complement":
-        S = oracle_mod.box_complement_excluded(a64, k) + oracle_mod.bdbs_included(a64, k)
+        S = oracle_mod.box_complement_excluded(a64, k)
     else:
         S = oracle_mod.bdbs_included(a64, k)
     return D * u * S + np.finfo(np.float64).tiny
