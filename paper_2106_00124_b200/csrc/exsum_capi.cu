@@ -898,9 +898,13 @@ int run_device_graph(int route, const void* in, void* out, int dtype, int op, in
   }
   const cudaGraphExec_t exec = hit->exec;
   const int launches = hit->launches;
-  lock.unlock();
   g_err.clear();
-  if (cudaGraphLaunch(exec, (cudaStream_t)stream) != cudaSuccess) return cuda_check("cudaGraphLaunch");
+  // launched under the cache lock (the launch is asynchronous and cheap): an
+  // eviction or exsum_release_cache on another thread cannot destroy `exec`
+  // between the lookup and the launch
+  const cudaError_t le = cudaGraphLaunch(exec, (cudaStream_t)stream);
+  lock.unlock();
+  if (le != cudaSuccess) return cuda_check("cudaGraphLaunch");
   g_last_launches = launches;
   g_total_launches += launches;
   return EXSUM_OK;
@@ -1333,12 +1337,19 @@ int exsum_route_host(int route, const void* h_in, void* h_out, int dtype, int op
       c.ws[slot].reserve(ws_bytes > 0 ? ws_bytes : 256))
     return fail(EXSUM_ECUDA, "cudaMalloc failed for host-path buffers");
   cudaStream_t st = c.stream[slot];
-  cudaMemcpyAsync(c.in[slot].p, h_in, bytes, cudaMemcpyHostToDevice, st);
-  rc = run_device(route, c.in[slot].p, c.out[slot].p, dtype, op, modulus, d, ext, box,
-                  c.ws[slot].p, c.ws[slot].cap, st);
+  // every exit below drains the stream first: no copy into or out of the
+  // caller's buffers may still be in flight when the call returns
+  if (cudaMemcpyAsync(c.in[slot].p, h_in, bytes, cudaMemcpyHostToDevice, st) != cudaSuccess) {
+    rc = cuda_check("cudaMemcpyAsync H2D");
+  } else {
+    rc = run_device(route, c.in[slot].p, c.out[slot].p, dtype, op, modulus, d, ext, box,
+                    c.ws[slot].p, c.ws[slot].cap, st);
+    if (!rc && cudaMemcpyAsync(h_out, c.out[slot].p, bytes, cudaMemcpyDeviceToHost, st) != cudaSuccess)
+      rc = cuda_check("cudaMemcpyAsync D2H");
+  }
+  const cudaError_t se = cudaStreamSynchronize(st);
   if (rc) return rc;
-  cudaMemcpyAsync(h_out, c.out[slot].p, bytes, cudaMemcpyDeviceToHost, st);
-  if (cudaStreamSynchronize(st) != cudaSuccess) return cuda_check("cudaStreamSynchronize");
+  if (se != cudaSuccess) return cuda_check("cudaStreamSynchronize");
   return cuda_check("host path");
 }
 
@@ -1387,22 +1398,38 @@ int exsum_route_host_batch(int route, int count, const void* const* h_in, void* 
     if (slot[k].in.reserve(bytes) || slot[k].out.reserve(bytes) ||
         slot[k].ws.reserve(ws_bytes > 0 ? ws_bytes : 256))
       return fail(EXSUM_ECUDA, "cudaMalloc failed for batch buffers");
-  for (int i = 0; i < count; ++i) {
+  // on any failure: stop issuing, then drain all three streams before
+  // returning, so no copy into or out of the caller's buffers is left in flight
+  auto step = [&](cudaError_t e, const char* what) {
+    if (e != cudaSuccess && !rc) rc = cuda_check(what);
+    return rc == 0;
+  };
+  for (int i = 0; i < count && !rc; ++i) {
     BatchSlot& b = slot[i % nslots];
-    if (i >= nslots) cudaStreamWaitEvent(s_in, b.done, 0);  // compute of i-2 released `in`
-    cudaMemcpyAsync(b.in.p, h_in[i], bytes, cudaMemcpyHostToDevice, s_in);
-    cudaEventRecord(b.h2d, s_in);
-    cudaStreamWaitEvent(s_run, b.h2d, 0);
-    if (i >= nslots) cudaStreamWaitEvent(s_run, b.d2h, 0);  // D2H of i-2 released `out`
+    if (i >= nslots && !step(cudaStreamWaitEvent(s_in, b.done, 0), "cudaStreamWaitEvent"))
+      break;  // compute of i-2 released `in`
+    if (!step(cudaMemcpyAsync(b.in.p, h_in[i], bytes, cudaMemcpyHostToDevice, s_in), "cudaMemcpyAsync H2D") ||
+        !step(cudaEventRecord(b.h2d, s_in), "cudaEventRecord") ||
+        !step(cudaStreamWaitEvent(s_run, b.h2d, 0), "cudaStreamWaitEvent"))
+      break;
+    if (i >= nslots && !step(cudaStreamWaitEvent(s_run, b.d2h, 0), "cudaStreamWaitEvent"))
+      break;  // D2H of i-2 released `out`
     rc = run_device(route, b.in.p, b.out.p, dtype, op, modulus, d, ext, box, b.ws.p, b.ws.cap,
                     s_run);
-    if (rc) return rc;
-    cudaEventRecord(b.done, s_run);
-    cudaStreamWaitEvent(s_out, b.done, 0);
-    cudaMemcpyAsync(h_out[i], b.out.p, bytes, cudaMemcpyDeviceToHost, s_out);
-    cudaEventRecord(b.d2h, s_out);
+    if (rc) break;
+    if (!step(cudaEventRecord(b.done, s_run), "cudaEventRecord") ||
+        !step(cudaStreamWaitEvent(s_out, b.done, 0), "cudaStreamWaitEvent") ||
+        !step(cudaMemcpyAsync(h_out[i], b.out.p, bytes, cudaMemcpyDeviceToHost, s_out), "cudaMemcpyAsync D2H") ||
+        !step(cudaEventRecord(b.d2h, s_out), "cudaEventRecord"))
+      break;
   }
-  if (cudaStreamSynchronize(s_out) != cudaSuccess) return cuda_check("cudaStreamSynchronize");
+  cudaError_t se = cudaSuccess;
+  for (cudaStream_t q : {s_in, s_run, s_out}) {
+    const cudaError_t e = cudaStreamSynchronize(q);
+    if (se == cudaSuccess) se = e;
+  }
+  if (rc) return rc;
+  if (se != cudaSuccess) return cuda_check("cudaStreamSynchronize");
   return cuda_check("host batch");
 }
 

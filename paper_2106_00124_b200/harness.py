@@ -39,7 +39,7 @@ from . import _native
 from .errors import ConfigurationError, UsageError
 from .monoid import device_operator, modulus_of, resolve_monoid, unwrap
 from .routes import ALGORITHMS, check_algorithm_config, resolve_algorithm
-from .tensor import Tensor, is_torch, load_text, normalize_box, validate_extents
+from .tensor import Tensor, is_torch, normalize_box, validate_extents
 
 CSV_HEADER = "algo,d,N,K,time_ns_per_elem,oplus_per_elem,peak_bytes_per_elem,verified"
 
@@ -183,7 +183,6 @@ def run_benchmark(
     delay_ns: int = 0,
     verify: bool = False,
     cache: int = 1,
-    input_path=None,
     device: str = "host",
 ) -> BenchResult:
     """Run one registry entry on one instance; median over ``trials`` runs
@@ -199,18 +198,13 @@ def run_benchmark(
         raise ConfigurationError("--delay-ns instruments a CPU operator; the B200 routes have none")
     if device not in ("host", "cuda"):
         raise ConfigurationError(f"device must be 'host' or 'cuda', got {device!r}")
-    if input_path is not None and extents is not None:
-        raise UsageError("give either extents or an input file, not both")
-    if input_path is None and extents is None:
-        raise UsageError("either extents or an input file is required")
+    if extents is None:
+        raise UsageError("extents are required")
     if box is None:
         raise UsageError("a box is required")
     check_algorithm_config(info, base_ops)  # monoid mismatch: fail before any work
-    if input_path is not None:
-        t_base = load_text(base_ops, input_path)
-    else:
-        check_algorithm_config(info, base_ops, len(validate_extents(extents)))
-        t_base = generate_input(base_ops, extents, seed)
+    check_algorithm_config(info, base_ops, len(validate_extents(extents)))
+    t_base = generate_input(base_ops, extents, seed)
     check_algorithm_config(info, base_ops, t_base.data.ndim)
     k = normalize_box(t_base.data.shape, box)
 

@@ -1,5 +1,7 @@
-"""The harness / CLI mirror: host logic on CPU, the
-end-to-end runs on the GPU (marked)."""
+"""The harness mirror: host logic on CPU, the end-to-end
+runs on the GPU (marked).  The command line is the reference's own
+(`exsum run/sweep` after `register_with_reference()`); this
+package ships no CLI of its own."""
 
 import csv
 import io
@@ -9,7 +11,7 @@ import pytest
 
 import paper_2106_00124_b200 as ex
 from golden_data import ext_cases, small_cases
-from paper_2106_00124_b200 import cli, harness
+from paper_2106_00124_b200 import harness
 
 
 def test_csv_header_matches_reference():
@@ -59,42 +61,20 @@ def test_brute_force_matches_reference_oracle():
     assert n >= 40
 
 
-def test_text_tensor_round_trip(tmp_path):
-    t = ex.Tensor(ex.FloatAddOps(), np.random.default_rng(1).random((3, 4)))
-    p = tmp_path / "t.txt"
-    ex.tensor.save_text(t, p)
-    back = ex.tensor.load_text(ex.FloatAddOps(), p)
-    assert back.data.tobytes() == t.data.tobytes()
-    p.write_text("2 2 2\n1\n2\n3\n")
+def test_harness_configuration_errors_before_work():
+    # every one of these fails before any device work (no GPU needed), with
+    # the reference's exception types (bench.check_algorithm_config)
+    for kw in (dict(algo="bdbsc", monoid="max-i64"), dict(algo="sat", monoid="max-i64"),
+               dict(algo="bdbs", monoid="mod-add:1"), dict(algo="naive-inc")):
+        algo = kw.pop("algo")
+        with pytest.raises(ex.ConfigurationError):
+            harness.run_benchmark(algo, extents=(4, 4), box=(2, 2), **kw)
     with pytest.raises(ex.UsageError):
-        ex.tensor.load_text(ex.IntAddOps(), p)
-
-
-def test_cli_configuration_errors_exit_2(capsys):
-    # every one of these fails before any device work (no GPU needed)
-    assert cli.main(["run", "--algo", "bdbsc", "--extents", "4,4", "--box", "2",
-                     "--monoid", "max-i64"]) == 2
-    assert cli.main(["run", "--algo", "sat", "--extents", "4,4", "--box", "2",
-                     "--monoid", "max-i64"]) == 2
-    assert cli.main(["run", "--algo", "bdbs", "--extents", "4,x", "--box", "2"]) == 2
-    assert cli.main(["run", "--algo", "bdbs", "--box", "2"]) == 2
-    assert cli.main(["run", "--algo", "bdbs", "--extents", "4,4", "--box", "2",
-                     "--monoid", "mod-add:1"]) == 2
-    assert cli.main(["run", "--algo", "bdbs", "--extents", "4,4", "--box", "2",
-                     "--trials", "0"]) == 2
-    assert cli.main(["run", "--algo", "bdbs", "--extents", "4,4", "--box", "2",
-                     "--delay-ns", "5"]) == 2
-    assert cli.main(["sweep", "--algos", "", "--dims", "2"]) == 2
-    assert cli.main(["sweep", "--algos", "bdbs", "--dims", "a:b"]) == 2
-    err = capsys.readouterr().err
-    assert "requires an invertible monoid" in err
-    # corners: 2-D / 3-D only (bench.check_algorithm_config dims), c in [1, d]
-    assert cli.main(["run", "--algo", "corners", "--extents", "4", "--box", "2"]) == 2
-    assert cli.main(["run", "--algo", "corners-spine", "--extents", "4,4,4,4", "--box", "2"]) == 2
-    assert cli.main(["run", "--algo", "corners", "--extents", "4,4", "--box", "2", "--c", "3"]) == 2
-    with pytest.raises(SystemExit) as e:
-        cli.main(["run", "--algo", "naive-inc", "--extents", "4", "--box", "2"])
-    assert e.value.code == 2
+        harness.run_benchmark("bdbs", extents=(4, 4), box=(2,))
+    with pytest.raises(ex.ConfigurationError):
+        harness.run_benchmark("corners", extents=(4,), box=(2,))
+    with pytest.raises(ex.ConfigurationError):
+        harness.run_benchmark("corners-spine", extents=(4, 4, 4, 4), box=(2, 2, 2, 2))
 
 
 @pytest.mark.gpu
@@ -111,17 +91,11 @@ def test_run_benchmark_verifies_every_route():
 
 
 @pytest.mark.gpu
-def test_cli_run_and_sweep(tmp_path, capsys):
-    target = tmp_path / "out.csv"
-    assert cli.main(["run", "--algo", "satc", "--extents", "6,6", "--box", "2", "--verify",
-                     "--csv", str(target)]) == 0
-    lines = target.read_text().splitlines()
-    assert lines[0] == harness.CSV_HEADER and lines[1].startswith("satc,2,36,4,")
-    assert lines[1].endswith(",pass")
-    assert cli.main(["sweep", "--algos", "bdbs,box-complement,sat", "--dims", "1:4",
-                     "--elems", "4096", "--trials", "1", "--device", "cuda"]) == 0
-    out = capsys.readouterr().out.strip().splitlines()
-    assert out[0] == harness.CSV_HEADER and len(out) == 1 + 3 * 4
+def test_run_sweep_rows():
+    rows = list(harness.run_sweep(["bdbs", "box-complement", "sat"], range(1, 5), target_elements=4096,
+                             trials=1))
+    assert len(rows) == 3 * 4 and all(r.time_ns > 0 for r in rows)
+    assert rows[0].csv_row().startswith("bdbs,1,")
     big = harness.run_benchmark("bdbs", extents=(17, 17, 15), box=(4, 4, 4), trials=1,
                                 verify=True)
     assert big.verified == "skipped"  # above VERIFY_ELEMENT_CAP, like the reference

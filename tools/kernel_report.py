@@ -2,8 +2,11 @@
 
     python tools/kernel_report.py [--configs c1,c2,c4,...] [--reps 3]
 
-Step time: CUDA events around back-to-back calls with the profiler off (graph
-replay on); per-kernel times: the library's CUDA-event profiler (exsum_profile_*), every launch
+Step time: CUDA events around each call with the profiler off (graph replay
+on); arrays under 4x the 126 MB L2 get a 512 MB L2 flush (a buffer write)
+before every timed call, outside its events, so no call reads its input from
+the previous call's L2 lines (the 4 GiB C4 arrays are 32x L2 and need none);
+per-kernel times: the library's CUDA-event profiler (exsum_profile_*), every launch
 bracketed by events on its own stream; bytes are the kernel's algorithmic
 (compulsory) bytes.  Prints one JSON object per (config, route).
 """
@@ -59,6 +62,26 @@ def main():
     peak = json.load(open(os.path.join(ROOT, "MEASURED_PEAKS.json")))["hbm_gbs"] \
         if os.path.exists(os.path.join(ROOT, "MEASURED_PEAKS.json")) else 6650.0
     dev = torch.device("cuda:0")
+    flush_buf = torch.empty(512 << 20, dtype=torch.uint8, device=dev)
+    L2_BYTES = 126 << 20
+
+    def timed(fn, t, box, reps, flush):
+        """Average device time of one call, each call bracketed by its own
+        events (after an L2 flush when `flush`)."""
+        total = 0.0
+        for _ in range(reps):
+            if flush:
+                flush_buf.zero_()
+            a = torch.cuda.Event(enable_timing=True)
+            b = torch.cuda.Event(enable_timing=True)
+            a.record()
+            o = fn(t, box)
+            b.record()
+            torch.cuda.synchronize()
+            total += a.elapsed_time(b)
+            del o
+        return total / reps
+
     for cname in args.configs.split(","):
         ext, dtype, boxes, routes = CASES[cname]
         g = torch.Generator(device=dev).manual_seed(0)
@@ -88,27 +111,12 @@ def main():
                 torch.cuda.synchronize()
                 # step time with the profiler off (its per-launch events cost
                 # 10-30% on the small configs, and it disables graph replay)
-                a0 = torch.cuda.Event(enable_timing=True)
-                b0 = torch.cuda.Event(enable_timing=True)
-                a0.record()
-                for _ in range(args.reps):
-                    o = fn(t, box)
-                    del o
-                b0.record()
-                torch.cuda.synchronize()
-                step_free = a0.elapsed_time(b0) / args.reps
+                flush = int(np.prod(ext)) * x.element_size() < 4 * L2_BYTES
+                step_free = timed(fn, t, box, args.reps, flush)
                 _native.profile_enable(True)
-                a = torch.cuda.Event(enable_timing=True)
-                b = torch.cuda.Event(enable_timing=True)
-                a.record()
-                for _ in range(args.reps):
-                    o = fn(t, box)
-                    del o
-                b.record()
-                torch.cuda.synchronize()
+                step_prof = timed(fn, t, box, args.reps, flush)
                 recs = _native.profile_records()
                 _native.profile_enable(False)
-                step_prof = a.elapsed_time(b) / args.reps
                 step_ms = step_free
                 per = {}
                 for name, by, ms in recs:
@@ -124,6 +132,7 @@ def main():
                 print(json.dumps({"config": cname, "route": route, "op": ops.name, "box": box,
                                   "step_ms": round(step_ms, 4),
                                   "step_ms_profiled": round(step_prof, 4),
+                                  "l2_flush": flush,
                                   "Gelem_s": round(N / step_ms / 1e6, 2),
                                   "compulsory_frac": round(2 * N * es / step_ms / 1e6 / peak, 3),
                                   "kernels": kern}), flush=True)
