@@ -135,16 +135,51 @@ class ClockSampler:
                 "samples": len(sms), "scope": scope}
 
 
-def make_input(cfg, device, seed=0, shape=None):
+def make_input(cfg, device, seed=0, shape=None, planes=None):
+    """The workload's seeded synthetic array, or planes [p0, p1) of it.
+
+    Every plane (index along axis 0) has its own Philox stream, seeded from
+    (seed, plane), so any slab of the global array -- a rank's own planes plus
+    its halo -- is generated exactly as the single-GPU array holds it: an N>1
+    run computes on slices of the one array the N=1 run sees.  `shape`
+    replaces the extents (its planes seeded the same way)."""
     import torch
 
     ext, dtype, box, dist, _ = CONFIGS[cfg]
-    shape = shape or ext
-    g = torch.Generator(device=device).manual_seed(seed)
-    if dist == "uniform01":
-        tdt = torch.float32 if dtype == "float32" else torch.float64
-        return torch.rand(shape, generator=g, device=device, dtype=tdt)
-    return torch.randint(-2**20, 2**20, shape, generator=g, device=device, dtype=torch.int64)
+    shape = tuple(shape or ext)
+    p0, p1 = planes if planes is not None else (0, shape[0])
+    tdt = {"float32": torch.float32, "float64": torch.float64, "int64": torch.int64}[dtype]
+    out = torch.empty((p1 - p0,) + shape[1:], dtype=tdt, device=device)
+    g = torch.Generator(device=device)
+    for p in range(p0, p1):
+        g.manual_seed((seed << 32) + p)
+        if dist == "uniform01":
+            torch.rand(shape[1:], generator=g, device=device, dtype=tdt, out=out[p - p0])
+        else:
+            torch.randint(-2**20, 2**20, shape[1:], generator=g, device=device, dtype=tdt,
+                          out=out[p - p0])
+    return out
+
+
+def bench_config(cfg, route, world, sharded_path):
+    """The `config` object of the JSON line -- identical in both arms."""
+    ext, dtype, box, dist, desc = CONFIGS[cfg]
+    es = 4 if dtype == "float32" else 8
+    N = int(np.prod(ext))
+    return {"workload": cfg, "description": desc, "extents": list(ext), "box": list(box),
+            "route": route, "operator": _monoid_name(dtype, route),
+            "parallelism": f"axis0-shards{world}" if sharded_path else "single-gpu",
+            "l2": "input 4 GiB >> 126 MB L2; no flush needed" if N * es > 2**30
+            else "input smaller than 4x L2",
+            "seed": 0}
+
+
+def _monoid_name(dtype, route):
+    if dtype == "float32":
+        return "add-f32"
+    if dtype == "float64":
+        return "add-f64"
+    return "max-i64" if route == "box-complement" else "add-i64"
 
 
 def ops_for(ex, dtype, route):
@@ -180,33 +215,72 @@ def cpu_sample(cfg, route, nthreads, planes=64, reps=1):
     return a.size / dt, shape, dt
 
 
+def _mem_available():
+    try:
+        for line in open("/proc/meminfo"):
+            if line.startswith("MemAvailable:"):
+                return int(line.split()[1]) * 1024
+    except OSError:
+        pass
+    return 0
+
+
 def run_reference(args, rank, world):
-    """--impl reference: the reference's CPU algorithm (oracle port) on host cores."""
+    """--impl reference: the reference's CPU algorithm on the host cores.
+
+    The reference is pure Python + numpy (single-threaded); its
+    algorithm restated in C with the reference's exact association
+    (oracle/exsum_oracle.c, OpenMP over independent lines and column tiles,
+    bit-identical for any thread count) runs here on every host thread.  A
+    step is the WHOLE workload array -- the same extents, box, route, value
+    distribution and seed as the GPU arm (same `config`); only if the host
+    lacks the memory for it does the step fall back to a leading-planes
+    sample, and `cpu_baseline.sample` says so.  Under torchrun only rank 0
+    runs."""
     if rank != 0:
         return
     cfg = args.config
     nthreads = os.cpu_count() or 1
     ext, dtype, box, _, desc = CONFIGS[cfg]
+    from oracle import oracle as orc
+
+    es = 4 if dtype == "float32" else 8
+    N = int(np.prod(ext))
+    # the oracle's box-complement holds 4 N-sized scratch arrays + out + in
+    need = 7 * N * es + (1 << 30)
+    planes = ext[0] if _mem_available() >= need else max(1, args.cpu_planes)
+    shape = (planes,) + tuple(ext[1:])
+    rng = np.random.default_rng(0)
+    if dtype == "int64":
+        a = rng.integers(-2**20, 2**20, size=shape, dtype=np.int64)
+    else:
+        a = rng.random(shape, dtype=np.float32 if dtype == "float32" else np.float64)
+    op = "max" if (dtype == "int64" and args.route == "box-complement") else "add"
+    fn = orc.ROUTES[args.route]
     for _ in range(args.warmup):
-        cpu_sample(cfg, args.route, nthreads, planes=args.cpu_planes)
-    vals, shape = [], None
+        fn(a, box, op, nthreads)
+    secs = []
     for _ in range(args.steps):
-        v, shape, _ = cpu_sample(cfg, args.route, nthreads, planes=args.cpu_planes)
-        vals.append(v)
-    value = statistics.median(vals)
-    n_step = int(np.prod(shape))
+        t0 = time.perf_counter()
+        fn(a, box, op, nthreads)
+        secs.append(time.perf_counter() - t0)
+    total = sum(secs)
+    value = a.size * args.steps / total
+    sample = (f"the whole {'x'.join(map(str, shape))} array every step" if planes == ext[0] else
+              f"the first {planes} planes ({'x'.join(map(str, shape))}) every step: the host "
+              f"lacks memory for the whole array")
     line = {
         "impl": "reference", "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world,
-        "steps": args.steps, "warmup": args.warmup, "ms_per_step": n_step / value * 1e3,
+        "steps": args.steps, "warmup": args.warmup, "ms_per_step": total / args.steps * 1e3,
         "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": _dt(dtype),
         "data": "synthetic",
-        "config": {"workload": cfg, "description": desc, "extents": list(ext), "box": list(box),
-                   "route": args.route},
+        "config": bench_config(cfg, args.route, world, world > 1 or args.sharded),
         "cpu_baseline": {"value": value, "unit": UNIT, "cores": nthreads, "kind": "port",
                          "cpu_model": _cpu_model(), "cpu_count": os.cpu_count(),
-                         "sample": f"{args.route} on the first {shape[0]} planes "
-                                   f"({'x'.join(map(str, shape))}) of the workload, "
-                                   f"oracle/exsum_oracle.c with {nthreads} OpenMP threads"},
+                         "sample": f"{args.route}: {sample}; oracle/exsum_oracle.c (the "
+                                   f"reference algorithm, its association) on {nthreads} "
+                                   f"OpenMP threads; values numpy default_rng(0)",
+                         "whole_array": planes == ext[0]},
         "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
     }
     print(json.dumps(line), flush=True)
@@ -240,6 +314,9 @@ def main():
     ap.add_argument("--cpu-planes", type=int, default=64)
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu", action="store_true")
+    ap.add_argument("--check", action="store_true",
+                    help="after timing, compare this rank's output planes with the single-GPU "
+                         "route on the whole global array (on this rank's GPU) and report it")
     ap.add_argument("--sharded", action="store_true",
                     help="use the multi-GPU (sharded, NCCL) path even at world size 1 "
                          "(run under torchrun; exercises the N>1 code on one GPU)")
@@ -274,7 +351,7 @@ def main():
     if sharded_path:
         from paper_2106_00124_b200 import sharded
 
-        x = sharded.make_local_slab(lambda shape: make_input(args.config, dev, shape=shape),
+        x = sharded.make_local_slab(lambda p0, p1: make_input(args.config, dev, planes=(p0, p1)),
                                     ext, rank, world, box)
         runner = sharded.ShardedRunner(args.route, ops, ext, box, rank, world, dev)
         step = lambda: runner(x)  # noqa: E731
@@ -469,6 +546,25 @@ def main():
                        "over ranks",
                "single_call_ms": sec1 * 1e3, "single_call_value": N / sec1}
 
+    check = None
+    if args.check:
+        # the sharded ranks hold slices of one seeded global array (make_input
+        # seeds every plane): their planes must equal the single-GPU route's
+        y = step()
+        full = make_input(args.config, dev)
+        ref = fn(ex.Tensor(ops, full), box).data
+        if sharded_path:
+            ref = ref[runner.start:runner.end]
+        diff = (y.double() - ref.double()).abs().max().item() if y is not None and y.numel() else 0.0
+        mag = ref.double().abs().max().item() if ref.numel() else 0.0
+        stats = torch.tensor([diff, mag], device=dev, dtype=torch.float64)
+        if dist is not None:
+            dist.all_reduce(stats, op=dist.ReduceOp.MAX)
+        check = {"against": "single-GPU route on the whole global array, each rank its planes",
+                 "max_abs_diff": stats[0].item(), "max_abs_value": stats[1].item(),
+                 "bit_exact": stats[0].item() == 0.0}
+        del y, full, ref
+
     cpu = None
     if not args.no_cpu and rank == 0 and world == 1:
         nthreads = os.cpu_count() or 1
@@ -485,11 +581,7 @@ def main():
             "warmup": args.warmup, "ms_per_step": ms_per_step, "higher_is_better": True,
             "scaling": "strong", "vs_baseline": None,  # the 1024^3 array is fixed as N grows
             "dtype": _dt(dtype), "data": "synthetic",
-            "config": {"workload": args.config, "description": desc, "extents": list(ext),
-                       "box": list(box), "route": args.route, "operator": ops.name,
-                       "parallelism": f"axis0-shards{world}" if sharded_path else "single-gpu",
-                       "l2": "input 4 GiB >> 126 MB L2; no flush needed" if N * es > 2**30
-                       else "input smaller than 4x L2"},
+            "config": bench_config(args.config, args.route, world, sharded_path),
             "roofline": roofline,
             "hbm_GBps_step": step_bytes / (ms_per_step / 1e3) / 1e9,
             "e2e_fraction_of_peak": e2e_frac,
@@ -500,6 +592,8 @@ def main():
             "e2e": e2e,
             "cpu_baseline": cpu,
         }
+        if check is not None:
+            line["check"] = check
         print(json.dumps(line), flush=True)
     if dist is not None:
         dist.destroy_process_group()

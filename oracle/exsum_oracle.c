@@ -41,6 +41,19 @@
 #define ORC_OK 0
 #define ORC_USAGE 1
 #define ORC_CONFIG 2
+/* column tile of the strided passes (elements) */
+#define ORC_TILE 256
+
+/* memcpy split over the OpenMP threads (large buffers: first touch and copy in parallel) */
+static void pcopy(void *dst, const void *src, size_t bytes) {
+    const size_t CH = (size_t)1 << 20;
+    int64_t nch = (int64_t)((bytes + CH - 1) / CH);
+    _Pragma("omp parallel for schedule(static)")
+    for (int64_t c = 0; c < nch; ++c) {
+        size_t o = (size_t)c * CH, b = bytes - o < CH ? bytes - o : CH;
+        memcpy((char *)dst + o, (const char *)src + o, b);
+    }
+}
 
 static int64_t prod_range(const int64_t *ext, int lo, int hi) {
     int64_t p = 1;
@@ -98,39 +111,95 @@ static inline int64_t i64_sub(int64_t a, int64_t b) { return (int64_t)((uint64_t
         }                                                                                      \
     }                                                                                          \
                                                                                                \
+    /* win_line_ on W adjacent lines at once (columns c of a strided axis): the same */      \
+    /* operations in the same order per column, walked row by row so every access */          \
+    /* is a contiguous run of W elements (cache lines used whole, vectorisable). */            \
+    static void win_tile_##SFX(T *buf, int64_t n, int64_t stride, int64_t k, int64_t W,       \
+                               T *scratch) {                                                   \
+        if (n == 0 || k == 1) return;                                                          \
+        if (k >= n) {                                                                          \
+            for (int64_t x = n - 2; x >= 0; --x) {                                             \
+                T *r = buf + x * stride; const T *q = r + stride;                              \
+                for (int64_t c = 0; c < W; ++c) r[c] = ACC(r[c], q[c]);                        \
+            }                                                                                  \
+            for (int64_t x = 0; x < n; ++x) {                                                  \
+                T *r = buf + x * stride;                                                       \
+                for (int64_t c = 0; c < W; ++c) r[c] = FIN(r[c]);                              \
+            }                                                                                  \
+            return;                                                                            \
+        }                                                                                      \
+        for (int64_t x = 0; x < n; ++x) memcpy(scratch + x * W, buf + x * stride, sizeof(T) * (size_t)W); \
+        for (int64_t bs = 0; bs < n; bs += k) {                                                \
+            int64_t be = bs + k < n ? bs + k : n;                                              \
+            for (int64_t x = be - 2; x >= bs; --x) {                                           \
+                T *r = buf + x * stride; const T *q = r + stride;                              \
+                for (int64_t c = 0; c < W; ++c) r[c] = C(r[c], q[c]);                          \
+            }                                                                                  \
+            for (int64_t x = bs + 1; x < be; ++x) {                                            \
+                T *r = scratch + x * W; const T *q = r - W;                                    \
+                for (int64_t c = 0; c < W; ++c) r[c] = C(r[c], q[c]);                          \
+            }                                                                                  \
+        }                                                                                      \
+        int64_t last_bs = k * ((n - 1) / k);                                                   \
+        for (int64_t x = 1; x < last_bs; ++x) {                                                \
+            if (x % k == 0) continue;                                                          \
+            int64_t p = x + k - 1 < n - 1 ? x + k - 1 : n - 1;                                 \
+            T *r = buf + x * stride; const T *q = scratch + p * W;                             \
+            for (int64_t c = 0; c < W; ++c) r[c] = C(r[c], q[c]);                              \
+        }                                                                                      \
+    }                                                                                          \
+                                                                                               \
     /* windowed_sum_axis over every line of a C-order array [outer, n, inner]. */             \
+    /* Contiguous lines (inner == 1) one per iteration; strided lines in tiles of */          \
+    /* ORC_TILE adjacent columns (bit-identical: every column keeps its own order). */        \
     static void pass_##SFX(T *data, int64_t outer, int64_t n, int64_t inner, int64_t k) {     \
         if (k == 1 || n == 0) return;                                                          \
-        int64_t lines = outer * inner;                                                         \
+        if (inner == 1) {                                                                      \
+            _Pragma("omp parallel")                                                            \
+            {                                                                                  \
+                T *scratch = (T *)malloc(sizeof(T) * (size_t)n);                               \
+                _Pragma("omp for schedule(static)")                                            \
+                for (int64_t o = 0; o < outer; ++o) win_line_##SFX(data + o * n, n, 1, k, scratch); \
+                free(scratch);                                                                 \
+            }                                                                                  \
+            return;                                                                            \
+        }                                                                                      \
+        int64_t tiles = (inner + ORC_TILE - 1) / ORC_TILE;                                     \
         _Pragma("omp parallel")                                                                \
         {                                                                                      \
-            T *scratch = (T *)malloc(sizeof(T) * (size_t)n);                                   \
+            T *scratch = (T *)malloc(sizeof(T) * (size_t)n * ORC_TILE);                        \
             _Pragma("omp for schedule(static)")                                                \
-            for (int64_t l = 0; l < lines; ++l) {                                              \
-                int64_t o = l / inner, i = l % inner;                                          \
-                win_line_##SFX(data + o * n * inner + i, n, inner, k, scratch);                \
+            for (int64_t l = 0; l < outer * tiles; ++l) {                                      \
+                int64_t o = l / tiles, c0 = (l % tiles) * ORC_TILE;                            \
+                int64_t W = inner - c0 < ORC_TILE ? inner - c0 : ORC_TILE;                     \
+                win_tile_##SFX(data + o * n * inner + c0, n, inner, k, W, scratch);            \
             }                                                                                  \
             free(scratch);                                                                     \
         }                                                                                      \
     }                                                                                          \
                                                                                                \
     /* np.add.accumulate / np.maximum.accumulate along axis 0 of [n, m] (forward or */        \
-    /* flipped); sequential per column like numpy. */                                         \
+    /* flipped); sequential per column like numpy, walked in column tiles. */                 \
     static void axis0_scan_##SFX(T *s, int64_t n, int64_t m, int reverse) {                    \
+        int64_t tiles = (m + ORC_TILE - 1) / ORC_TILE;                                         \
         _Pragma("omp parallel for schedule(static)")                                           \
-        for (int64_t c = 0; c < m; ++c) {                                                      \
+        for (int64_t t = 0; t < tiles; ++t) {                                                  \
+            int64_t c0 = t * ORC_TILE, c1 = c0 + ORC_TILE < m ? c0 + ORC_TILE : m;             \
             if (!reverse) {                                                                    \
-                for (int64_t x = 1; x < n; ++x) s[x * m + c] = ACC(s[(x - 1) * m + c], s[x * m + c]); \
+                for (int64_t x = 1; x < n; ++x)                                                \
+                    for (int64_t c = c0; c < c1; ++c) s[x * m + c] = ACC(s[(x - 1) * m + c], s[x * m + c]); \
             } else {                                                                           \
-                for (int64_t x = n - 2; x >= 0; --x) s[x * m + c] = ACC(s[(x + 1) * m + c], s[x * m + c]); \
+                for (int64_t x = n - 2; x >= 0; --x)                                           \
+                    for (int64_t c = c0; c < c1; ++c) s[x * m + c] = ACC(s[(x + 1) * m + c], s[x * m + c]); \
             }                                                                                  \
-            for (int64_t x = 0; x < n; ++x) s[x * m + c] = FIN(s[x * m + c]);                  \
+            for (int64_t x = 0; x < n; ++x)                                                    \
+                for (int64_t c = c0; c < c1; ++c) s[x * m + c] = FIN(s[x * m + c]);            \
         }                                                                                      \
     }                                                                                          \
                                                                                                \
     static void bdbs_##SFX(const T *in, T *out, int d, const int64_t *ext, const int64_t *k) { \
         int64_t N = prod_range(ext, 0, d);                                                     \
-        memcpy(out, in, sizeof(T) * (size_t)N);                                                \
+        pcopy(out, in, sizeof(T) * (size_t)N);                                                 \
         for (int a = 0; a < d; ++a)                                                            \
             pass_##SFX(out, prod_range(ext, 0, a), ext[a], prod_range(ext, a + 1, d), k[a]);   \
     }                                                                                          \
@@ -151,7 +220,7 @@ static inline int64_t i64_sub(int64_t a, int64_t b) { return (int64_t)((uint64_t
         int64_t lo = offset < 0 ? -offset : 0;                                                 \
         int64_t hi = n - offset < n ? n - offset : n;                                          \
         if (lo >= hi) return;                                                                  \
-        _Pragma("omp parallel for schedule(static)")                                           \
+        _Pragma("omp parallel for collapse(2) schedule(static)")                               \
         for (int64_t o = 0; o < outer; ++o)                                                    \
             for (int64_t x = lo; x < hi; ++x) {                                                \
                 T *dst = out + (o * n + x) * inner;                                            \
@@ -170,21 +239,21 @@ static inline int64_t i64_sub(int64_t a, int64_t b) { return (int64_t)((uint64_t
             free(cur); free(nxt); free(win); free(pre);                                        \
             return ORC_USAGE;                                                                  \
         }                                                                                      \
-        for (int64_t i = 0; i < N; ++i) out[i] = (T)(IDENT);                                   \
-        memcpy(cur, in, sizeof(T) * (size_t)N);                                                \
+        _Pragma("omp parallel for schedule(static)")                                           \
+        for (int64_t i = 0; i < N; ++i) { out[i] = (T)(IDENT); cur[i] = in[i]; }               \
         for (int i = 0; i < d; ++i) {                                                          \
             /* reduced_slice: dims < i pinned at their last index (scan.py:105-110) */        \
             int64_t off = 0, stride = N;                                                       \
             for (int j = 0; j < i; ++j) { stride /= ext[j]; off += (ext[j] - 1) * stride; }    \
             int64_t M = prod_range(ext, i, d), ni = ext[i], m = M / ni;                        \
             if (i < d - 1) {                                                                   \
-                memcpy(nxt + off, cur + off, sizeof(T) * (size_t)M);                           \
+                pcopy(nxt + off, cur + off, sizeof(T) * (size_t)M);                           \
                 axis0_scan_##SFX(nxt + off, ni, m, 0);                                         \
             }                                                                                  \
-            memcpy(win + off, cur + off, sizeof(T) * (size_t)M);                               \
+            pcopy(win + off, cur + off, sizeof(T) * (size_t)M);                               \
             for (int j = i + 1; j < d; ++j)                                                    \
                 pass_##SFX(win + off, prod_range(ext, i, j), ext[j], prod_range(ext, j + 1, d), k[j]); \
-            memcpy(pre + off, win + off, sizeof(T) * (size_t)M);                               \
+            pcopy(pre + off, win + off, sizeof(T) * (size_t)M);                               \
             axis0_scan_##SFX(pre + off, ni, m, 0);                                             \
             add_contribution_##SFX(pre + off, out, d, ext, i, -1);                             \
             axis0_scan_##SFX(win + off, ni, m, 1);                                             \

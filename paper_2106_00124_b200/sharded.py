@@ -181,13 +181,14 @@ class CudaEngine:
 class DistComm:
     """Halo exchange and all-gathers over torch.distributed (NCCL or gloo)."""
 
-    def __init__(self, rank, world, device=None):
+    def __init__(self, rank, world, device=None, grouped=True):
         import torch.distributed as dist
 
         self.dist = dist
         self.rank = rank
         self.world = world
         self.nccl = dist.get_backend() == "nccl"
+        self.grouped = grouped
 
     def exchange_halo(self, plan, x_ext, n_own):
         """Blocking form of start_halo()."""
@@ -219,10 +220,21 @@ class DistComm:
             ops.append(dist.P2POp(dist.irecv, recv, src))
         if not ops:
             return []
-        # plain non-blocking isend / irecv on every backend: the gloo tests run
-        # exactly this code, and unlike batch_isend_irecv it has no requirement
-        # that every rank take part in the first batch (a rank may own no planes)
+        if self.grouped and self._all_ranks_exchange(plan):
+            # every rank takes part (the first and last ranks with one side
+            # each): one grouped exchange, posted together (NCCL group)
+            return dist.batch_isend_irecv(ops)
+        # some rank owns no planes and would post nothing: a grouped call must
+        # see every rank, so fall back to plain non-blocking isend / irecv
         return [(dist.isend if o.op is dist.isend else dist.irecv)(o.tensor, o.peer) for o in ops]
+
+    def _all_ranks_exchange(self, plan):
+        """True when every rank posts at least one halo send or receive."""
+        if self.world < 2:
+            return False
+        if any(e <= s for s, e in (plan.bounds(q) for q in range(self.world))):
+            return False
+        return all(plan.halo(q) > 0 for q in range(self.world - 1))
 
     def all_gather_rows(self, t, counts):
         """Concatenate per-rank tensors of `counts[q]` rows along axis 0."""
@@ -430,12 +442,16 @@ def run_loopback(route, ops, a, box, world, engine, split=True):
     return torch.cat(outs, dim=0)
 
 
-def make_local_slab(gen, ext, rank, world, box=None):
-    """Allocate this rank's slab (own planes + halo room) and fill the own planes
-    with gen(shape); the halo is filled by the exchange."""
+def make_local_slab(gen_planes, ext, rank, world, box=None):
+    """Allocate this rank's slab (own planes + halo room) and fill the own
+    planes with gen_planes(p0, p1) -- planes [p0, p1) of the GLOBAL array, so
+    the ranks together hold exactly the array one GPU would see (and an N>1
+    run can be checked against it).  The halo is filled by the exchange."""
     plan, _ = plan_for(ext, box if box is not None else (1,) * len(ext), world)
     start, end = plan.bounds(rank)
-    own = gen((end - start,) + tuple(ext[1:]))
+    own = gen_planes(start, end)
+    if tuple(own.shape) != (end - start,) + tuple(ext[1:]):
+        raise UsageError(f"gen_planes({start}, {end}) returned shape {tuple(own.shape)}")
     halo = plan.halo(rank)
     if halo == 0:
         return own

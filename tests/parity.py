@@ -22,8 +22,13 @@ Exactness contract (north star):
         (+ sum(|A|) for satc's total) and D = sum_i(n_i) + 2^d + 8.  Where the
         scans run unsegmented the float tables are bit-identical to the
         reference's (numpy's sequential accumulate), and so is sat itself.
-    The float64 oracle's own error is D_ref * 2^-53 * S, negligible next to
-    float32's u = 2^-24; for float64 data both sides count.
+    Both sides round: tau * S(x) = (D_gpu * u + D_ref * 2^-53) * S(x), the
+    oracle always running in float64 (tau = (D_gpu + D_ref) u).
+    D_ref follows the reference's own association: BDBS sum_i(2 k_i - 1),
+    BDBSC N + sum_i(2 k_i) (its total is one sequential fold over all N
+    elements, monoid.py:200-204), box-complement sum_i(n_i - 1) + sum_i(2 k_i)
+    + 2d.  Next to float32's u = 2^-24 the oracle's share is negligible
+    except for BDBSC's sequential total; for float64 data it matters.
 """
 
 from __future__ import annotations
@@ -43,14 +48,22 @@ def depth(route, ext, k):
     return sum(n + 2 * kk for n, kk in zip(ext, k)) + 16
 
 
+def depth_ref(route, ext, k):
+    """Rounding depth of the reference's own association."""
+    if route == "bdbs":
+        return sum(2 * kk - 1 for kk in k)
+    if route == "bdbsc":
+        return int(np.prod(ext)) + sum(2 * kk for kk in k)
+    if route in ("sat", "satc"):
+        return depth(route, ext, k)
+    return sum(n - 1 for n in ext) + sum(2 * kk for kk in k) + 2 * len(ext)
+
+
 def float_tolerance(route, a, k, oracle_mod):
     """Elementwise tolerance array for a float route (see module docstring)."""
     ext = a.shape
-    u = U[np.dtype(a.dtype)]
-    if np.dtype(a.dtype) == np.float64:
-        u = 2 * u  # both sides round in float64
     a64 = np.abs(a.astype(np.float64))
-    D = depth(route, ext, k)
+    tau = depth(route, ext, k) * U[np.dtype(a.dtype)] + depth_ref(route, ext, k) * 2.0**-53
     if route == "bdbsc":
         S = np.full(ext, a64.sum())
     elif route in ("sat", "satc"):
@@ -59,7 +72,7 @@ def float_tolerance(route, a, k, oracle_mod):
         S = oracle_mod.box_complement_excluded(a64, k)
     else:
         S = oracle_mod.bdbs_included(a64, k)
-    return D * u * S + np.finfo(np.float64).tiny
+    return tau * S + np.finfo(np.float64).tiny
 
 
 def compare(route, got, want, a, k, oracle_mod):

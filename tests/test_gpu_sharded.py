@@ -60,3 +60,68 @@ def test_loopback_matches_single_gpu(ext, box, mono, world):
         if ops.dtype.kind == "i":
             op = "max" if mono == "max-i64" else "add"
             assert np.array_equal(sharded, orc.ROUTES[route](a, box, op)), route
+
+
+def _nccl_world1_worker(port, q):
+    """One process, NCCL process group of world size 1 on cuda:0: the real
+    DistComm (NCCL all-gathers, rank-order totals) and CudaEngine stages."""
+    import os
+    import sys
+    import traceback
+
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    sys.path[:0] = [root, os.path.join(root, "tests")]
+    try:
+        import torch
+        import torch.distributed as dist
+
+        import bench
+        import paper_2106_00124_b200 as ex
+        from oracle import oracle as orc
+        from paper_2106_00124_b200.sharded import ShardedRunner, make_local_slab
+        from parity import compare, float64_oracle
+
+        dev = torch.device("cuda", 0)
+        torch.cuda.set_device(dev)
+        dist.init_process_group("nccl", init_method=f"tcp://127.0.0.1:{port}", rank=0,
+                                world_size=1, device_id=dev)
+        assert dist.get_backend() == "nccl"
+        ext, box = (64, 96, 1024), (16, 16, 16)
+        for route, mono in (("box-complement", "add-f32"), ("bdbsc", "add-f32"),
+                            ("bdbs", "add-f32"), ("box-complement", "max-i64")):
+            ops = ex.resolve_monoid(mono)
+            cfg = "c4" if mono == "add-f32" else "c2"
+            x = make_local_slab(lambda p0, p1: bench.make_input(cfg, dev, shape=ext, planes=(p0, p1)),
+                                ext, 0, 1, box)
+            runner = ShardedRunner(route, ops, ext, box, 0, 1, dev)
+            got = runner(x).cpu().numpy()
+            a = x.cpu().numpy()
+            op = "max" if mono == "max-i64" else "add"
+            # bdbs: bit-exact against the oracle in the data's own type
+            want = (orc.ROUTES[route](a, box, op) if route == "bdbs"
+                    else float64_oracle(route, a, box, orc, op))
+            ok, ratio, rel = compare(route, got, want, a, box, orc)
+            assert ok, (route, mono, ratio, rel)
+        dist.destroy_process_group()
+        q.put("ok")
+    except Exception:  # pragma: no cover - reported to the parent
+        q.put(traceback.format_exc())
+
+
+def test_nccl_world1_sharded_routes():
+    """the NCCL code path of ShardedRunner (world size 1 -- the
+    GPU boxes of this run have one GPU) against the oracle for all routes."""
+    import socket
+
+    import torch.multiprocessing as mp
+
+    with socket.socket() as sk:
+        sk.bind(("127.0.0.1", 0))
+        port = sk.getsockname()[1]
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    p = ctx.Process(target=_nccl_world1_worker, args=(port, q))
+    p.start()
+    msg = q.get(timeout=600)
+    p.join(timeout=60)
+    assert msg == "ok", msg

@@ -39,6 +39,7 @@ def _worker(rank, world, init_file, q):
     from oracle import oracle as orc
     from paper_2106_00124_b200 import resolve_monoid
     from paper_2106_00124_b200.sharded import DistComm, ShardedRunner, make_local_slab
+    from parity import float_tolerance
     from shard_engines import OracleEngine
 
     dist.init_process_group("gloo", init_method=f"file://{init_file}", rank=rank,
@@ -56,8 +57,8 @@ def _worker(rank, world, init_file, q):
             engine = OracleEngine(op, np.dtype(dt).name)
             runner = ShardedRunner(route, ops, ext, box, rank, world, torch.device("cpu"),
                                    comm=DistComm(rank, world), engine=engine)
-            x = make_local_slab(lambda shape: torch.from_numpy(
-                a[runner.start:runner.start + shape[0]].copy()), ext, rank, world, box)
+            x = make_local_slab(lambda p0, p1: torch.from_numpy(a[p0:p1].copy()), ext, rank,
+                                world, box)
             out = runner(x)
             if route == "box-complement" or (route == "bdbsc" and np.dtype(dt).kind == "f"):
                 src = a.astype(np.float64) if np.dtype(dt).kind == "f" else a
@@ -69,8 +70,10 @@ def _worker(rank, world, init_file, q):
                 continue
             got = out.numpy()
             if np.dtype(dt).kind == "f" and route != "bdbs":
-                tol = 1e-5 * np.abs(a).astype(np.float64).sum()
-                assert np.max(np.abs(got.astype(np.float64) - want)) <= tol, (ci, route)
+                # the exactness contract of tests/parity.py on this rank's planes
+                k = tuple(min(b, n) for b, n in zip(box, ext))
+                tol = float_tolerance(route, a, k, orc)[runner.start:runner.end]
+                assert np.all(np.abs(got.astype(np.float64) - want) <= tol), (ci, route)
             else:
                 assert np.array_equal(got, want.astype(got.dtype)), (ci, route, rank)
         q.put((rank, "ok"))
@@ -82,8 +85,8 @@ def _worker(rank, world, init_file, q):
         dist.destroy_process_group()
 
 
-def test_sharded_world2_gloo():
-    world = 2
+@pytest.mark.parametrize("world", [2, 3])
+def test_sharded_gloo(world):
     ctx = mp.get_context("spawn")
     q = ctx.Queue()
     with tempfile.TemporaryDirectory() as td:
@@ -109,3 +112,18 @@ def test_slab_plan():
     assert all(b[0] % 4 == 0 for b in (p.bounds(r) for r in range(3)))
     p = SlabPlan(5, 5, 2)
     assert p.bounds(1) == (5, 5) and p.halo(0) == 0
+
+
+def test_grouped_halo_only_when_every_rank_posts():
+    """batch_isend_irecv needs every rank in the group: it is used only when
+    every rank owns planes and every rank but the last receives a halo."""
+    from paper_2106_00124_b200.sharded import DistComm, SlabPlan
+
+    c = DistComm.__new__(DistComm)
+    c.grouped = True
+    for world, plan, want in ((8, SlabPlan(1024, 16, 8), True), (2, SlabPlan(37, 4, 2), True),
+                              (2, SlabPlan(5, 5, 2), False),     # rank 1 owns nothing
+                              (3, SlabPlan(37, 1, 3), False),    # k0 = 1: no halo at all
+                              (1, SlabPlan(64, 16, 1), False)):
+        c.world = world
+        assert c._all_ranks_exchange(plan) is want, (world, plan)

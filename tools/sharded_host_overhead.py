@@ -13,7 +13,7 @@ torch.cuda.set_device(dev)
 dist.init_process_group("nccl", device_id=dev)
 for route in ("box-complement", "bdbsc", "bdbs"):
     ext, box = (128, 1024, 1024), (16, 16, 16)
-    x = sharded.make_local_slab(lambda s: torch.rand(s, device=dev), ext, 0, 1, box)
+    x = sharded.make_local_slab(lambda p0, p1: torch.rand((p1 - p0,) + ext[1:], device=dev), ext, 0, 1, box)
     r = sharded.ShardedRunner(route, ex.Float32AddOps(), ext, box, 0, 1, dev)
     for _ in range(5):
         r(x)
