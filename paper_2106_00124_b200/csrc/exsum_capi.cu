@@ -451,6 +451,25 @@ int route_box_complement(const Shape& s, int dtype, int op, const void* src, voi
     t.k[i] = s.k[i];
   }
   auto reduce_and_tail = [&]() -> int {
+    if (d == 3 && tail2d_ok(dtype, s.ext[0], s.ext[1], s.k[0])) {
+      // R is 2-D: R (from the row partials), its fold R2 and T = BC(R) in
+      // two launches (tail2d.cu)
+      void* R2 = ar.take((size_t)s.ext[0] * es);
+      if (!live) return EXSUM_OK;
+      if (!ex0.done) {
+        ProfScope ps("row_reduce", (double)(s.N + rows) * es, st);
+        *launches += launch_row_reduce(dtype, op, src, R, rows, n, st);
+      }
+      for (int stage = 0; stage < 2; ++stage) {
+        ProfScope ps(stage ? "tail_group" : "tail_rows",
+                     (double)(stage ? 2 : (ex0.done ? ex0.ppr + 1 : 1)) * rows * es, st);
+        const int rc = launch_tail2d(dtype, op, ex0.done ? ex0.buf : nullptr, ex0.ppr, R, R2, T,
+                                     s.ext[0], s.ext[1], s.k[0], s.k[1], st, stage);
+        if (rc < 0) return fail(EXSUM_ECONFIG, "no tail kernel for this dtype/operator");
+        *launches += rc;
+      }
+      return EXSUM_OK;
+    }
     if (live) {
       if (ex0.done) {
         *launches += launch_rowpart_final(dtype, op, ex0.buf, R, rows, ex0.ppr, st);

@@ -58,6 +58,14 @@ int launch_total(int dtype, int op, const void* in, int64_t N, void* partials, v
 int launch_complement(int dtype, const void* in, void* out, int64_t N, const void* total,
                       cudaStream_t s);
 
+// Box-complement tail of a 3-D array (tail2d.cu): R (n0 x n1) from row
+// partials part[ppr][n0*n1] (or, part == nullptr, R as given), R2 (n0) its
+// fold over the last axis, Tout = BC(R, (k0, k1)).  stage 0 writes R and R2,
+// stage 1 (after it) writes Tout; one launch each.
+int tail2d_ok(int dtype, int64_t n0, int64_t n1, int64_t k0);
+int launch_tail2d(int dtype, int op, const void* part, int64_t ppr, void* R, void* R2, void* Tout,
+                  int64_t n0, int64_t n1, int64_t k0, int64_t k1, cudaStream_t s, int stage);
+
 // R[r] = (+)_x in[r, x] for rows of length n (box-complement reduction of the
 // peeled last axis).
 int launch_row_reduce(int dtype, int op, const void* in, void* R, int64_t rows, int64_t n,
