@@ -48,6 +48,9 @@ CONFIGS = {
            "C2 3-D excluded sums, int64 256^3 uniform[-2^20,2^20), box 8^3"),
     "c1": ((1024, 1024), "float64", (32, 32), "uniform01",
            "C1 2-D included sum, float64 1024^2 uniform[0,1), box 32^2"),
+    # C5 (box/aspect sweep) -- a measurement target for tools/, not a bench line
+    "c5": ((512, 512, 512), "float64", (8, 8, 8), "normal",
+           "C5 3-D box sweep, float64 512^3 standard normal, box 8^3"),
 }
 METRIC = "box-sum elements/s"
 UNIT = "elements/s"
@@ -155,6 +158,8 @@ def make_input(cfg, device, seed=0, shape=None, planes=None):
         g.manual_seed((seed << 32) + p)
         if dist == "uniform01":
             torch.rand(shape[1:], generator=g, device=device, dtype=tdt, out=out[p - p0])
+        elif dist == "normal":
+            torch.randn(shape[1:], generator=g, device=device, dtype=tdt, out=out[p - p0])
         else:
             torch.randint(-2**20, 2**20, shape[1:], generator=g, device=device, dtype=tdt,
                           out=out[p - p0])
