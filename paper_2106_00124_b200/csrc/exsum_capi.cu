@@ -396,6 +396,23 @@ int route_box_complement(const Shape& s, int dtype, int op, const void* src, voi
   const int d = s.d;
   const int64_t n = s.ext[d - 1];
   const int64_t rows = s.N / n;
+  if (idem_max_ok(dtype, op, d, s.ext)) {
+    // max is idempotent: the per-axis marginal form (idem_max.cu), one read
+    // and one write of the array
+    size_t bytes = 0;
+    launch_idem_max(dtype, src, dst, d, s.ext, s.k, nullptr, &bytes, st, -1);
+    void* ws = ar.take(bytes);
+    if (!live) return EXSUM_OK;
+    static const char* names[2] = {"idem_scan", "idem_bcast"};
+    for (int stage = 0; stage < 2; ++stage) {
+      const double b = (double)s.N * es;
+      ProfScope ps(names[stage], b, st);
+      const int rc = launch_idem_max(dtype, src, dst, d, s.ext, s.k, ws, nullptr, st, stage);
+      if (rc < 0) return fail(EXSUM_ECONFIG, "no marginal kernel for this dtype");
+      *launches += rc;
+    }
+    return EXSUM_OK;
+  }
   if (d == 1) {
     void* scratch = ar.take(excl_rows_scratch_elems(dtype, 1, n) * es);
     if (live) {

@@ -90,6 +90,17 @@ int launch_fused_pair(int dtype, int op, const void* in, void* out, int64_t oute
                       int64_t n2, int64_t k1, int64_t k2, int mode, const void* total,
                       const void* Tail, cudaStream_t s);
 
+// Box-complement for max as per-axis marginals (idem_max.cu): out[x] =
+// (+)_a F_a[x_a], F_a the 1-D excluded window of the marginal M_a (the fold over
+// every axis but a) -- exact for an idempotent operator.  idem_max_ok() decides
+// eligibility (EXSUM_IDEM=0 disables); launch_idem_max(stage): -1 sizes the
+// workspace only (*ws_bytes), 0 the marginals and tables (one read of A), 1 the
+// broadcast (one write of out).
+#define EXSUM_IDEM_MAX_DIMS 32
+int idem_max_ok(int dtype, int op, int d, const int64_t* ext);
+int launch_idem_max(int dtype, const void* in, void* out, int d, const int64_t* ext,
+                    const int64_t* k, void* ws, size_t* ws_bytes, cudaStream_t st, int stage);
+
 // Trailing-block fusion (block_fused.cu): the windowed passes along the last m
 // axes in one kernel when a block of those axes (last axis padded to an odd
 // length) fits in shared memory.  block_fused_plan picks the largest such m

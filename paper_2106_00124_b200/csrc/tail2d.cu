@@ -120,7 +120,8 @@ k_tail_rows(const T* __restrict__ part, int64_t ppr, T* __restrict__ R, T* __res
 //    S[x + k1] and T1 (out-of-range terms the identity), staged back and
 //    stored coalesced.
 constexpr int kGroup = 4;
-constexpr int kGroupThreads = 32 * kGroup;
+constexpr int kGroupThreads = 256;  // the W phase and the folds; warps < kGroup run the row round
+constexpr int kGroupWarps = kGroupThreads / 32;
 
 template <int C>
 __device__ __forceinline__ int poff(int x) { return (x / C) * (C + 1) + (x % C); }
@@ -136,7 +137,7 @@ __device__ __forceinline__ T group_fold(T v, T* sh) {
   __syncthreads();
   T t = sh[0];
 #pragma unroll
-  for (int w = 1; w < kGroup; ++w) t = Op::apply(t, sh[w]);
+  for (int w = 1; w < kGroupWarps; ++w) t = Op::apply(t, sh[w]);
   return t;
 }
 
@@ -149,7 +150,7 @@ k_tail_group(const T* __restrict__ R, const T* __restrict__ R2, T* __restrict__ 
   __shared__ __align__(16) T Wt[G][P];
   __shared__ __align__(16) T Sr[G][P];
   __shared__ T t1[G];
-  __shared__ T sh[G];
+  __shared__ T sh[kGroupWarps];
   const T ident = Op::template identity<T>();
   const int lane = threadIdx.x & 31;
   const int warp = threadIdx.x >> 5;
@@ -177,41 +178,62 @@ k_tail_group(const T* __restrict__ R, const T* __restrict__ R2, T* __restrict__ 
     // ---- W rows of the group ----
     if (gk == G && gm == G) {
       const int mid_e = g0 + k0 < n0 ? g0 + k0 : n0;   // middle [g0+G-1, mid_e)
-      for (int c = threadIdx.x; c < n1; c += blockDim.x) {
-        const T* col = R + c;
-        T a[G - 1], bq[G - 1];
+      const int mid_s = g0 + G - 1;
+      // CW columns per thread at a time, every load of them issued before the
+      // folds (the middle in batches of MB rows)
+      constexpr int CW = 2;
+      constexpr int MB = 16;
+      for (int cb = threadIdx.x; cb < n1; cb += CW * blockDim.x) {
+        T a[CW][G - 1], bq[CW][G - 1], mv[CW];
 #pragma unroll
-        for (int j = 0; j < G - 1; ++j) a[j] = col[(int64_t)(g0 + j) * n1];
+        for (int u = 0; u < CW; ++u) {
+          const int c = cb + u * blockDim.x;
+          const bool ok = c < n1;
+          const T* col = R + (ok ? c : 0);
 #pragma unroll
-        for (int j = 0; j < G - 1; ++j)
-          bq[j] = mid_e + j < n0 ? col[(int64_t)(mid_e + j) * n1] : ident;
-        T mv = ident;
-        constexpr int MB = 8;  // middle rows per batch of loads
-        for (int y0 = g0 + G - 1; y0 < mid_e; y0 += MB) {
-          T q[MB];
+          for (int j = 0; j < G - 1; ++j) a[u][j] = ok ? col[(int64_t)(g0 + j) * n1] : ident;
 #pragma unroll
-          for (int j = 0; j < MB; ++j) q[j] = y0 + j < mid_e ? col[(int64_t)(y0 + j) * n1] : ident;
-#pragma unroll
-          for (int j = 0; j < MB; ++j) mv = Op::apply(mv, q[j]);
+          for (int j = 0; j < G - 1; ++j)
+            bq[u][j] = ok && mid_e + j < n0 ? col[(int64_t)(mid_e + j) * n1] : ident;
+          mv[u] = ident;
         }
-        // A_j: suffix over in-group rows j..G-2; B_j: prefix over the G-1 rows past the middle
-        T w[G];
-        T run = mv;
-        w[G - 1] = mv;
+        for (int y0 = mid_s; y0 < mid_e; y0 += MB) {
+          T q[CW][MB];
 #pragma unroll
-        for (int j = G - 2; j >= 0; --j) {
-          run = Op::apply(a[j], run);
-          w[j] = run;
+          for (int u = 0; u < CW; ++u) {
+            const int c = cb + u * blockDim.x;
+#pragma unroll
+            for (int j = 0; j < MB; ++j)
+              q[u][j] = (c < n1 && y0 + j < mid_e) ? R[(int64_t)(y0 + j) * n1 + c] : ident;
+          }
+#pragma unroll
+          for (int u = 0; u < CW; ++u)
+#pragma unroll
+            for (int j = 0; j < MB; ++j) mv[u] = Op::apply(mv[u], q[u][j]);
         }
-        T bp = ident;
 #pragma unroll
-        for (int j = 1; j < G; ++j) {
-          bp = Op::apply(bp, bq[j - 1]);  // rows [mid_e, mid_e + j) (identity past n0)
-          w[j] = Op::apply(w[j], bp);
+        for (int u = 0; u < CW; ++u) {
+          const int c = cb + u * blockDim.x;
+          if (c >= n1) continue;
+          // A_j: suffix over in-group rows j..G-2; B_j: prefix over the G-1 rows past the middle
+          T w[G];
+          T run = mv[u];
+          w[G - 1] = mv[u];
+#pragma unroll
+          for (int j = G - 2; j >= 0; --j) {
+            run = Op::apply(a[u][j], run);
+            w[j] = run;
+          }
+          T bp = ident;
+#pragma unroll
+          for (int j = 1; j < G; ++j) {
+            bp = Op::apply(bp, bq[u][j - 1]);  // rows [mid_e, mid_e + j) (identity past n0)
+            w[j] = Op::apply(w[j], bp);
+          }
+          const int po = poff<C>(c);
+#pragma unroll
+          for (int j = 0; j < G; ++j) Wt[j][po] = w[j];
         }
-        const int po = poff<C>(c);
-#pragma unroll
-        for (int j = 0; j < G; ++j) Wt[j][po] = w[j];
       }
     } else {
       // a short last group or k0 < G: each row's window directly
