@@ -327,6 +327,11 @@ def main():
                          "(run under torchrun; exercises the N>1 code on one GPU)")
     args = ap.parse_args()
 
+    if args.sharded and "RANK" not in os.environ:
+        # --sharded without torchrun: a world of one rank on this host
+        os.environ.update({"RANK": "0", "LOCAL_RANK": "0", "WORLD_SIZE": "1",
+                           "MASTER_ADDR": "127.0.0.1",
+                           "MASTER_PORT": os.environ.get("MASTER_PORT", "29531")})
     rank = int(os.environ.get("RANK", "0"))
     world = int(os.environ.get("WORLD_SIZE", "1"))
     if args.impl == "reference":
