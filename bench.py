@@ -386,6 +386,11 @@ def main():
     if dist is not None:
         dist.barrier()
     torch.cuda.synchronize(dev)
+    # keep the GPU busy while the host enqueues the K steps (~0.2 ms of spin per
+    # step, before the first start event): the events then time the device's
+    # back-to-back execution of the steps, not the host's enqueue rate -- which
+    # bounds a small config (C1: ~16 us of Python per call), and which e2e keeps
+    torch.cuda._sleep(int(args.steps * 2e-4 * 1.965e9))
     t_begin = time.time()
     launches0 = _native.total_launch_count()
     for i in range(args.steps):

@@ -419,7 +419,12 @@ int go_bulk(const T* in, T* out, int64_t outer, int64_t n, int64_t inner, int64_
   // enough warps in flight: ~8 per SM, at least 2 blocks per segment
   const int64_t want = (int64_t)num_sms() * 8;
   int64_t nseg = (want + lines - 1) / lines;
-  int64_t max_seg = nblocks / 2;
+#ifndef TMA_SMALL_SEG
+#define TMA_SMALL_SEG 0
+#endif
+  // segments of >= 2 blocks bound the halo re-reads; an array too small to
+  // fill the machine that way may take one-block segments
+  int64_t max_seg = (TMA_SMALL_SEG && lines * (nblocks / 2) < want) ? nblocks : nblocks / 2;
   if (max_seg < 1) max_seg = 1;
   if (nseg > max_seg) nseg = max_seg;
   if (nseg < 1) nseg = 1;
@@ -505,7 +510,12 @@ int go_tma(const T* in, T* out, int64_t outer, int64_t n, int64_t inner, int64_t
   const int64_t nblocks = (n + k - 1) / k;
   const int64_t want = (int64_t)num_sms() * 8;
   int64_t nseg = (want + lines - 1) / lines;
-  int64_t max_seg = nblocks / 2;
+#ifndef TMA_SMALL_SEG
+#define TMA_SMALL_SEG 0
+#endif
+  // segments of >= 2 blocks bound the halo re-reads; an array too small to
+  // fill the machine that way may take one-block segments
+  int64_t max_seg = (TMA_SMALL_SEG && lines * (nblocks / 2) < want) ? nblocks : nblocks / 2;
   if (max_seg < 1) max_seg = 1;
   if (nseg > max_seg) nseg = max_seg;
   if (nseg < 1) nseg = 1;

@@ -72,6 +72,9 @@ def main():
         for _ in range(reps):
             if flush:
                 flush_buf.zero_()
+            # the GPU spins while the host enqueues the call: the events time
+            # the device, not the host's launch overhead (small configs)
+            torch.cuda._sleep(400000)
             a = torch.cuda.Event(enable_timing=True)
             b = torch.cuda.Event(enable_timing=True)
             a.record()

@@ -38,6 +38,7 @@ for i in range(reps):
     if flush is not None: flush.sum()
     torch.cuda.synchronize()
     _native.profile_enable(True)
+    torch.cuda._sleep(400000)  # the device spins while the host enqueues the call
     a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     a.record(); o = fn(t, box); b.record(); torch.cuda.synchronize()
     steps.append(a.elapsed_time(b))
@@ -48,6 +49,7 @@ for i in range(reps):
 plain = []
 for i in range(reps):
     if flush is not None: flush.sum()
+    torch.cuda._sleep(400000)
     a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     a.record(); o = fn(t, box); b.record(); torch.cuda.synchronize()
     plain.append(a.elapsed_time(b)); del o
