@@ -289,12 +289,20 @@ int route_bdbs(const Shape& s, int dtype, int op, const void* in, void* out, Are
   const bool fused = p.count >= 2 && p.axes[p.count - 2] == d - 2 && p.axes[p.count - 1] == d - 1 &&
                      fused_pair_ok(dtype, op, s.ext[d - 1], s.k[d - 2], s.k[d - 1], ROW_WIN) &&
                      aligned16(out) && (p.count > 2 || aligned16(in));
+  // windows the fused pair has no template for (k = 32) on small arrays: the
+  // last two passes as one tiled kernel (tile_pair.cu)
+  const bool tilep = !fused && p.count >= 2 && p.axes[p.count - 2] == d - 2 &&
+                     p.axes[p.count - 1] == d - 1 &&
+                     tile_pair_ok(dtype, op, s.N, s.ext[d - 2], s.ext[d - 1], s.k[d - 2],
+                                  s.k[d - 1]) &&
+                     aligned16(out) && (p.count > 2 || aligned16(in));
   PassPlan head = p;
-  if (fused) head.count -= 2;
+  if (fused || tilep) head.count -= 2;
   // otherwise the trailing axes as one shared-memory block when it fits
   // (block_fused.cu): the passes along axes >= d - m in one HBM round trip
   BlockSpec bsp;
-  const bool blockf = !fused && p.count >= 2 && block_fused_plan(dtype, d, s.ext, s.k, 0, &bsp);
+  const bool blockf =
+      !fused && !tilep && p.count >= 2 && block_fused_plan(dtype, d, s.ext, s.k, 0, &bsp);
   if (blockf) {
     head.count = 0;
     while (head.count < p.count && p.axes[head.count] < d - bsp.m) ++head.count;
@@ -305,7 +313,7 @@ int route_bdbs(const Shape& s, int dtype, int op, const void* in, void* out, Are
   ex0.buf = partials;
   ex0.cap = reduce_partials_count();
   const bool piggy =
-      complement && !given_total && head.count >= 1 && (fused || blockf || head.count >= 2);
+      complement && !given_total && head.count >= 1 && (fused || tilep || blockf || head.count >= 2);
   if (complement && !piggy) full_total();
   auto finish_total = [&]() -> int {
     if (piggy && live) {
@@ -319,7 +327,7 @@ int route_bdbs(const Shape& s, int dtype, int op, const void* in, void* out, Are
   };
   const void* mid = in;
   if (head.count > 0) {
-    const bool tail_kernel = fused || blockf;
+    const bool tail_kernel = fused || tilep || blockf;
     void* head_dst = tail_kernel ? other : out;
     void* head_other = tail_kernel ? out : other;
     int rc = run_chain(s, head, dtype, op, in, head_dst, head_other, tail_kernel ? nullptr : total,
@@ -331,6 +339,14 @@ int route_bdbs(const Shape& s, int dtype, int op, const void* in, void* out, Are
     ProfScope ps("block_fused", 2.0 * (double)s.N * es, st);
     int rc = launch_block_fused(dtype, op, mid, out, s.N, bsp, total, st);
     if (rc < 0) return fail(EXSUM_ECONFIG, "no block kernel for this dtype/operator");
+    *launches += rc;
+  }
+  if (tilep && live) {
+    ProfScope ps("tile_pair", 2.0 * (double)s.N * es, st);
+    const int64_t n1 = s.ext[d - 2], n2 = s.ext[d - 1];
+    int rc = launch_tile_pair(dtype, op, mid, out, s.N / (n1 * n2), n1, n2, s.k[d - 2], s.k[d - 1],
+                              total, st);
+    if (rc < 0) return fail(EXSUM_ECUDA, "tiled pass pair failed to launch");
     *launches += rc;
   }
   if (fused && live) {

@@ -101,6 +101,15 @@ int idem_max_ok(int dtype, int op, int d, const int64_t* ext);
 int launch_idem_max(int dtype, const void* in, void* out, int d, const int64_t* ext,
                     const int64_t* k, void* ws, size_t* ws_bytes, cudaStream_t st, int stage);
 
+// The last two windowed passes of BDBS (windows k1 == k2 == 32) in one launch
+// over shared-memory tiles with their stitch halos (tile_pair.cu); total !=
+// nullptr applies the BDBSC complement epilogue.  tile_pair_ok() decides
+// eligibility (EXSUM_TILE_PAIR=0 disables; arrays of at most 64 MB: on larger
+// ones the two streaming passes are faster).
+int tile_pair_ok(int dtype, int op, int64_t N, int64_t n1, int64_t n2, int64_t k1, int64_t k2);
+int launch_tile_pair(int dtype, int op, const void* in, void* out, int64_t outer, int64_t n1,
+                     int64_t n2, int64_t k1, int64_t k2, const void* total, cudaStream_t s);
+
 // Trailing-block fusion (block_fused.cu): the windowed passes along the last m
 // axes in one kernel when a block of those axes (last axis padded to an odd
 // length) fits in shared memory.  block_fused_plan picks the largest such m
