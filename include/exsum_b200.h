@@ -212,6 +212,24 @@ int exsum_box_complement_finish(const void *in, void *out, int dtype, int op, in
                                 const int64_t *ext, const int64_t *box, const void *tail,
                                 void *ws, size_t ws_bytes, void *stream);
 
+/* Box-complement for max (int64) as per-axis marginals, sharded along axis 0
+ * (no halo: the ranks all-reduce sum(ext) values).  ext is the GLOBAL extents;
+ * a rank holds global planes [x0, x0 + n_own).
+ * exsum_shard_idem_marginals: the rank's marginals M_a[i] (max over the
+ *   rank's elements with coordinate i on axis a; INT64_MIN where it has none)
+ *   into marg (sum(ext) int64, device); workspace sum(ext) * 8 bytes.
+ * exsum_shard_idem_write: the rank's output planes from the all-reduced
+ *   (elementwise max over ranks) marginals.
+ * EXSUM_ECONFIG when the form does not apply (not max-i64, d < 2 or
+ * sum(ext) > 4096): run the slab stages above instead. */
+int exsum_shard_idem_workspace_bytes(int dtype, int op, int d, const int64_t *ext, size_t *bytes);
+int exsum_shard_idem_marginals(const void *in, void *marg, int dtype, int op, int d,
+                               const int64_t *ext, int64_t x0, int64_t n_own, void *ws,
+                               size_t ws_bytes, void *stream);
+int exsum_shard_idem_write(const void *marg, void *out, int dtype, int op, int d,
+                           const int64_t *ext, const int64_t *box, int64_t x0, int64_t n_own,
+                           void *stream);
+
 #ifdef __cplusplus
 }
 #endif

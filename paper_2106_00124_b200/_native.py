@@ -29,6 +29,9 @@ ABI_VERSION = 2
 EXPORTS = (
     "exsum_abi_version",
     "exsum_last_error",
+    "exsum_shard_idem_workspace_bytes",
+    "exsum_shard_idem_marginals",
+    "exsum_shard_idem_write",
     "exsum_workspace_bytes",
     "exsum_route_workspace_bytes",
     "exsum_route",
@@ -129,6 +132,12 @@ def load():
             fn = getattr(L, name)
             fn.argtypes = [vp, vp, ci, ci, ci, i64p, i64p, vp, vp, sz, vp]
             fn.restype = ci
+        L.exsum_shard_idem_workspace_bytes.argtypes = [ci, ci, ci, i64p, ctypes.POINTER(sz)]
+        L.exsum_shard_idem_workspace_bytes.restype = ci
+        L.exsum_shard_idem_marginals.argtypes = [vp, vp, ci, ci, ci, i64p, i64, i64, vp, sz, vp]
+        L.exsum_shard_idem_marginals.restype = ci
+        L.exsum_shard_idem_write.argtypes = [vp, vp, ci, ci, ci, i64p, i64p, i64, i64, vp]
+        L.exsum_shard_idem_write.restype = ci
         if L.exsum_abi_version() != ABI_VERSION:
             raise DeviceError("libexsum_b200.so ABI version mismatch")
         _lib = L

@@ -1657,6 +1657,71 @@ int exsum_bdbs_finish(const void* in, void* out, int dtype, int op, int d, const
                           stream);
 }
 
+// ---- box-complement for max as marginals, sharded along axis 0 (idem_max.cu) ----
+static int idem_shard_check(int dtype, int op, int d, const int64_t* ext, int64_t x0,
+                            int64_t n_own) {
+  int rc = check_types(dtype, op);
+  if (rc) return rc;
+  if (d < 1 || d > EXSUM_MAX_DIMS || !ext) return fail(EXSUM_EUSAGE, "bad extents");
+  for (int i = 0; i < d; ++i)
+    if (ext[i] < 1) return fail(EXSUM_EUSAGE, "every extent must be >= 1");
+  if (x0 < 0 || n_own < 0 || x0 + n_own > ext[0]) return fail(EXSUM_EUSAGE, "planes out of range");
+  if (!idem_max_ok(dtype, op, d, ext))
+    return fail(EXSUM_ECONFIG, "the marginal form needs max over int64, d >= 2 and sum(ext) <= 4096");
+  return EXSUM_OK;
+}
+
+int exsum_shard_idem_workspace_bytes(int dtype, int op, int d, const int64_t* ext, size_t* bytes) {
+  g_err.clear();
+  int rc = idem_shard_check(dtype, op, d, ext, 0, 0);
+  if (rc) return rc;
+  int64_t S = 0;
+  for (int i = 0; i < d; ++i) S += ext[i];
+  if (bytes) *bytes = (size_t)S * 8;
+  return EXSUM_OK;
+}
+
+int exsum_shard_idem_marginals(const void* in, void* marg, int dtype, int op, int d,
+                               const int64_t* ext, int64_t x0, int64_t n_own, void* ws,
+                               size_t ws_bytes, void* stream) {
+  g_err.clear();
+  int rc = idem_shard_check(dtype, op, d, ext, x0, n_own);
+  if (rc) return rc;
+  if (!marg || (n_own > 0 && !in)) return fail(EXSUM_EUSAGE, "null buffer");
+  size_t need = 0;
+  int64_t k1[EXSUM_MAX_DIMS];
+  for (int i = 0; i < d; ++i) k1[i] = 1;
+  launch_idem_max_shard(dtype, in, nullptr, marg, d, ext, k1, x0, n_own, nullptr, &need, nullptr, -1);
+  if (!ws || ws_bytes < need) return fail(EXSUM_EUSAGE, "workspace too small (see exsum_shard_idem_workspace_bytes)");
+  const int n = launch_idem_max_shard(dtype, in, nullptr, marg, d, ext, k1, x0, n_own, ws, nullptr,
+                                      (cudaStream_t)stream, 0);
+  if (n < 0) return fail(EXSUM_ECUDA, "marginal kernels failed to launch");
+  g_last_launches = n;
+  g_total_launches += n;
+  return cuda_check("shard marginals");
+}
+
+int exsum_shard_idem_write(const void* marg, void* out, int dtype, int op, int d, const int64_t* ext,
+                           const int64_t* box, int64_t x0, int64_t n_own, void* stream) {
+  g_err.clear();
+  int rc = idem_shard_check(dtype, op, d, ext, x0, n_own);
+  if (rc) return rc;
+  Shape sh;
+  rc = normalize(d, ext, box, &sh);
+  if (rc) return rc;
+  if (!marg || (n_own > 0 && !out)) return fail(EXSUM_EUSAGE, "null buffer");
+  if (n_own == 0) {
+    g_last_launches = 0;
+    return EXSUM_OK;
+  }
+  const int n = launch_idem_max_shard(dtype, nullptr, out, const_cast<void*>(marg), d, ext, sh.k, x0,
+                                      n_own, nullptr, nullptr, (cudaStream_t)stream, 1);
+  if (n < 0) return fail(EXSUM_ECUDA, "broadcast kernel failed to launch");
+  g_last_launches = n;
+  g_total_launches += n;
+  return cuda_check("shard broadcast");
+}
+
 int exsum_box_complement_finish(const void* in, void* out, int dtype, int op, int d,
                                 const int64_t* ext, const int64_t* box, const void* tail,
                                 void* ws, size_t ws_bytes, void* stream) {

@@ -100,6 +100,12 @@ int launch_fused_pair(int dtype, int op, const void* in, void* out, int64_t oute
 int idem_max_ok(int dtype, int op, int d, const int64_t* ext);
 int launch_idem_max(int dtype, const void* in, void* out, int d, const int64_t* ext,
                     const int64_t* k, void* ws, size_t* ws_bytes, cudaStream_t st, int stage);
+// A shard (global planes [x0, x0 + n_own) of axis 0; ext global): stage 0 the
+// shard's marginals as plain values into marg (S = sum of ext), stage 1 the
+// shard's output planes from the all-reduced marginals; -1 sizes ws.
+int launch_idem_max_shard(int dtype, const void* in, void* out, void* marg, int d,
+                          const int64_t* ext, const int64_t* k, int64_t x0, int64_t n_own,
+                          void* ws, size_t* ws_bytes, cudaStream_t st, int stage);
 
 // The last two windowed passes of BDBS (windows k1 == k2 == 32) in one launch
 // over shared-memory tiles with their stitch halos (tile_pair.cu); total !=

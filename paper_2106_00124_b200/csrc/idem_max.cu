@@ -62,8 +62,9 @@ struct IdemShape {
   int64_t ext[EXSUM_IDEM_MAX_DIMS];
   int64_t k[EXSUM_IDEM_MAX_DIMS];
   int64_t off[EXSUM_IDEM_MAX_DIMS];  // table offset of axis a (sum of the extents before it)
-  int64_t rows, nl;                  // rows = N / n_{d-1}, nl = n_{d-1}
+  int64_t rows, nl;                  // rows held here (a shard: its own), nl = n_{d-1}
   int64_t S;                         // sum of the extents
+  int64_t row_off;                   // global index of the first row held here (a shard's)
 };
 
 // The marginals accumulate with atomic max on the order-preserving unsigned
@@ -196,7 +197,7 @@ k_idem_scan(const T* __restrict__ in, unsigned long long* __restrict__ Mu, IdemS
     // rows with equal r / stride_a form contiguous lane segments; a segmented
     // suffix fold leaves each segment's fold in its first lane, which issues
     // one atomic (C2 axis 0: one atomic per warp instead of 32 on one address)
-    int64_t key = r0 + lane;  // r / stride_a, axis by axis from the last
+    int64_t key = s.row_off + r0 + lane;  // global row / stride_a, axis by axis from the last
     for (int a = s.d - 2; a >= 0; --a) {
       T v = lane < nr ? rmax : ident;
 #pragma unroll
@@ -235,7 +236,7 @@ k_idem_scan(const T* __restrict__ in, unsigned long long* __restrict__ Mu, IdemS
 template <class T, class Op, int VE, int NV>
 __global__ void __launch_bounds__(kIdemThreads)
 k_idem_bcast(const unsigned long long* __restrict__ Mu, T* __restrict__ out, IdemShape s,
-             int64_t nstrip, int64_t nrb) {
+             int64_t nstrip, int64_t nrb, unsigned long long flip) {
   typedef Vec<T, VE> VT;
   constexpr int W = 32 * VE * NV;
   extern __shared__ __align__(16) unsigned char smem[];
@@ -243,7 +244,8 @@ k_idem_bcast(const unsigned long long* __restrict__ Mu, T* __restrict__ out, Ide
   T* Ss = F + s.S;                    // [S]: inclusive suffixes
   const T ident = Op::template identity<T>();
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-  for (int64_t i = tid; i < s.S; i += kIdemThreads) F[i] = unbias(Mu[i]);
+  // the marginals: biased images (flip = sign bit) or, for a shard, plain values (flip = 0)
+  for (int64_t i = tid; i < s.S; i += kIdemThreads) F[i] = (T)(Mu[i] ^ flip);
   __syncthreads();
   for (int a = warp; a < s.d; a += kIdemWarps) {
     const int n = (int)s.ext[a];
@@ -286,7 +288,7 @@ k_idem_bcast(const unsigned long long* __restrict__ Mu, T* __restrict__ out, Ide
   const int nr = (int)min((int64_t)kRbu, s.rows - r0);
   T crow = ident;
   if (lane < nr) {
-    int64_t r = r0 + lane;
+    int64_t r = s.row_off + r0 + lane;
     for (int a = s.d - 2; a >= 0; --a) {
       const int64_t q = r / s.ext[a];
       crow = Op::apply(crow, F[s.off[a] + (r - q * s.ext[a])]);
@@ -319,30 +321,34 @@ k_idem_bcast(const unsigned long long* __restrict__ Mu, T* __restrict__ out, Ide
 // stage -1: workspace bytes only; 0: memset + scan, 1: broadcast (with the tables)
 template <class T, class Op, int VE, int NV>
 void launch_stage(const T* in, T* out, const IdemShape& s, const IdemTiling& t,
-                  unsigned long long* Mu, cudaStream_t st, int stage) {
+                  unsigned long long* Mu, cudaStream_t st, int stage, unsigned long long flip) {
   const unsigned grid = (unsigned)t.ncta;
   if (stage == 0) {
     k_idem_scan<T, Op, VE, NV><<<grid, kIdemThreads, 0, st>>>(in, Mu, s, t.nstrip, t.nrb);
   } else {
     const size_t sm = (size_t)2 * s.S * sizeof(T);
     ensure_smem((const void*)k_idem_bcast<T, Op, VE, NV>, sm);
-    k_idem_bcast<T, Op, VE, NV><<<grid, kIdemThreads, sm, st>>>(Mu, out, s, t.nstrip, t.nrb);
+    k_idem_bcast<T, Op, VE, NV><<<grid, kIdemThreads, sm, st>>>(Mu, out, s, t.nstrip, t.nrb, flip);
   }
 }
 
+// stage 2 (a shard): the broadcast from plain marginals `marg` (the all-reduced
+// global ones) instead of the workspace's biased images
 template <class T, class Op>
 int go_idem(const T* in, T* out, const IdemShape& s, void* ws, cudaStream_t st, int stage,
-            size_t* bytes) {
+            size_t* bytes, const void* marg = nullptr) {
   const bool vec = s.nl % 2 == 0 && ((uintptr_t)in % 16) == 0 && ((uintptr_t)out % 16) == 0 &&
                    sizeof(T) == 8;
   const IdemTiling t = idem_tiling(s, vec);
   // workspace: Mu [S], the marginals' biased images
   if (bytes) *bytes = (size_t)s.S * 8;
   if (stage < 0) return 0;
-  unsigned long long* Mu = static_cast<unsigned long long*>(ws);
+  unsigned long long* Mu = stage == 2 ? (unsigned long long*)marg : static_cast<unsigned long long*>(ws);
+  const unsigned long long flip = stage == 2 ? 0ULL : 0x8000000000000000ULL;
+  if (stage == 2) stage = 1;
   // the marginals start at zero (= the identity's image)
   if (stage == 0 && cudaMemsetAsync(Mu, 0, (size_t)s.S * 8, st) != cudaSuccess) return -1;
-#define IDEM_GO(VE_, NV_) launch_stage<T, Op, VE_, NV_>(in, out, s, t, Mu, st, stage)
+#define IDEM_GO(VE_, NV_) launch_stage<T, Op, VE_, NV_>(in, out, s, t, Mu, st, stage, flip)
   if (t.VE == 2) {
     switch (t.NV) {
       case 1: IDEM_GO(2, 1); break;
@@ -362,6 +368,13 @@ int go_idem(const T* in, T* out, const IdemShape& s, void* ws, cudaStream_t st, 
   return 1;
 }
 
+__global__ void k_idem_unbias(const unsigned long long* __restrict__ Mu, i64* __restrict__ marg,
+                              int64_t S) {
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < S;
+       i += (int64_t)gridDim.x * blockDim.x)
+    marg[i] = unbias(Mu[i]);
+}
+
 }  // namespace
 
 int idem_max_ok(int dtype, int op, int d, const int64_t* ext) {
@@ -375,6 +388,51 @@ int idem_max_ok(int dtype, int op, int d, const int64_t* ext) {
   int64_t S = 0;
   for (int a = 0; a < d; ++a) S += ext[a];
   return S <= kIdemMaxSum ? 1 : 0;
+}
+
+// A shard of the global array: `in` / `out` hold global planes [x0, x0 + n_own)
+// of axis 0.  stage 0: the shard's marginals as plain values into `marg`
+// (S = sum of the global extents; the identity where the shard has no
+// element), through the biased images in `ws`; stage 1: the shard's output
+// planes from the all-reduced global marginals `marg`.
+int launch_idem_max_shard(int dtype, const void* in, void* out, void* marg, int d,
+                          const int64_t* ext, const int64_t* k, int64_t x0, int64_t n_own,
+                          void* ws, size_t* ws_bytes, cudaStream_t st, int stage) {
+  if (dtype != I64) return -1;
+  IdemShape s;
+  s.d = d;
+  s.S = 0;
+  int64_t per_plane = 1;
+  for (int a = 0; a < d; ++a) {
+    s.ext[a] = ext[a];
+    s.k[a] = k[a];
+    s.off[a] = s.S;
+    s.S += ext[a];
+    if (a > 0) per_plane *= ext[a];
+  }
+  s.nl = ext[d - 1];
+  const int64_t rows_per_plane = per_plane / s.nl;
+  s.rows = n_own * rows_per_plane;
+  s.row_off = x0 * rows_per_plane;
+  if (stage < 0 || s.rows == 0) {
+    if (ws_bytes) *ws_bytes = (size_t)s.S * 8;
+    if (stage >= 0 && s.rows == 0 && stage == 0) {
+      // no planes here: every marginal entry is the identity
+      if (cudaMemsetAsync(ws, 0, (size_t)s.S * 8, st) != cudaSuccess) return -1;
+      k_idem_unbias<<<(unsigned)((s.S + 255) / 256), 256, 0, st>>>(
+          static_cast<const unsigned long long*>(ws), static_cast<i64*>(marg), s.S);
+      return 1;
+    }
+    return 0;
+  }
+  if (stage == 0) {
+    int rc = go_idem<i64, OpMax>(static_cast<const i64*>(in), nullptr, s, ws, st, 0, ws_bytes);
+    if (rc < 0) return rc;
+    k_idem_unbias<<<(unsigned)((s.S + 255) / 256), 256, 0, st>>>(
+        static_cast<const unsigned long long*>(ws), static_cast<i64*>(marg), s.S);
+    return rc + 1;
+  }
+  return go_idem<i64, OpMax>(nullptr, static_cast<i64*>(out), s, nullptr, st, 2, ws_bytes, marg);
 }
 
 int launch_idem_max(int dtype, const void* in, void* out, int d, const int64_t* ext,
@@ -393,6 +451,7 @@ int launch_idem_max(int dtype, const void* in, void* out, int d, const int64_t* 
   }
   s.nl = ext[d - 1];
   s.rows = N / s.nl;
+  s.row_off = 0;
   return go_idem<i64, OpMax>(static_cast<const i64*>(in), static_cast<i64*>(out), s, ws, st, stage,
                              ws_bytes);
 }

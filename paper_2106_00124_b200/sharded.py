@@ -17,6 +17,12 @@ cross-rank data are:
   small array redundantly and keeps its own rows.
 
 Everything else (the remaining windowed passes, the row round) is local.
+
+Box-complement with max over int64 (an idempotent operator) takes the
+per-axis marginal form instead (csrc/idem_max.cu): every rank folds its own
+planes into the sum(ext) marginals, the ranks all-reduce them (elementwise
+max), and every rank writes its planes from the global marginals -- no halo
+and no tail, one read and one write of each rank's planes.
 Per rank at the C4 shape and 8 GPUs: ~1/8 of 4 GiB of HBM traffic per pass vs
 a 60 MB halo and a 4 MB all-gather over NVLink.
 
@@ -157,6 +163,42 @@ class CudaEngine:
             self._stream()))
         return out
 
+    def idem_ok(self, ext):
+        """Whether the per-axis marginal form applies (max over int64, d >= 2,
+        sum of the extents within the kernel's tables)."""
+        import ctypes
+
+        if self.op != "max":
+            return False
+        out = ctypes.c_size_t(0)
+        rc = self.L.exsum_shard_idem_workspace_bytes(
+            _native.DTYPE[self.dtype_name], _native.OP[self.op], len(ext), _native.i64_array(ext),
+            ctypes.byref(out))
+        self._idem_ws = int(out.value)
+        return rc == 0
+
+    def idem_marginals(self, x_own, ext, x0):
+        """This rank's marginals (sum(ext) int64; the identity where it holds no element)."""
+        torch = self.torch
+        S = int(sum(ext))
+        marg = torch.empty(S, dtype=torch.int64, device=self.device)
+        ws = self._workspace(self._idem_ws)
+        n_own = int(x_own.shape[0])
+        _native.check(self.L.exsum_shard_idem_marginals(
+            x_own.data_ptr() if n_own else None, marg.data_ptr(), _native.DTYPE[self.dtype_name],
+            _native.OP[self.op], len(ext), _native.i64_array(ext), int(x0), n_own, ws.data_ptr(),
+            ws.numel(), self._stream()))
+        return marg
+
+    def idem_write(self, marg, ext, box, x0, n_own):
+        torch = self.torch
+        out = torch.empty((n_own,) + tuple(ext[1:]), dtype=torch.int64, device=self.device)
+        _native.check(self.L.exsum_shard_idem_write(
+            marg.data_ptr(), out.data_ptr() if n_own else None, _native.DTYPE[self.dtype_name],
+            _native.OP[self.op], len(ext), _native.i64_array(ext), _native.i64_array(box), int(x0),
+            int(n_own), self._stream()))
+        return out
+
     def box_complement(self, a, box):
         from .routes import run_device
 
@@ -256,6 +298,11 @@ class DistComm:
         self.dist.all_gather(bufs, t)
         return bufs
 
+    def all_reduce_max(self, t):
+        """Elementwise max over the ranks, in place."""
+        self.dist.all_reduce(t, op=self.dist.ReduceOp.MAX)
+        return t
+
 
 def combine_totals(totals, is_int):
     """Rank-order fold of the per-rank totals (deterministic)."""
@@ -299,6 +346,9 @@ class ShardedRunner:
         self.start, self.end = self.plan.bounds(rank)
         self.n_own = self.end - self.start
         self.halo = self.plan.halo(rank)
+        # max over int64: the per-axis marginal form -- no halo, no tail
+        self.idem = (route == "box-complement" and op == "max" and hasattr(self.engine, "idem_ok")
+                     and self.engine.idem_ok(self.ext))
 
     def local_shape(self):
         return (self.n_own + self.halo,) + self.ext[1:]
@@ -306,6 +356,11 @@ class ShardedRunner:
     def __call__(self, x_ext):
         if tuple(x_ext.shape) != self.local_shape():
             raise UsageError(f"slab shape {tuple(x_ext.shape)} != {self.local_shape()}")
+        if self.idem:
+            # the halo room (if any) stays unused: the marginal form needs none
+            marg = self.engine.idem_marginals(x_ext[:self.n_own], self.ext, self.start)
+            marg = self.comm.all_reduce_max(marg)
+            return self.engine.idem_write(marg, self.ext, self.k, self.start, self.n_own)
         reqs = self.comm.start_halo(self.plan, x_ext, self.n_own)
         y, extra = self.stage1(x_ext, reqs)
         combined = self.combine(extra, x_ext.device)
@@ -400,6 +455,11 @@ class _LoopbackComm:
         self.world = world
         self.extras = None
 
+    def all_reduce_max(self, t):
+        import torch
+
+        return torch.stack(self.extras).amax(dim=0)
+
     def all_gather_scalars(self, t):
         return self.extras
 
@@ -425,6 +485,12 @@ def run_loopback(route, ops, a, box, world, engine, split=True):
     comm = _LoopbackComm(world)
     runners = [ShardedRunner(route, ops, ext, box, r, world, a.device, comm=comm, engine=engine)
                for r in range(world)]
+    if runners and runners[0].idem:
+        comm.extras = [engine.idem_marginals(a[r.start:r.end].contiguous(), ext, r.start)
+                       for r in runners]
+        marg = comm.all_reduce_max(None)
+        outs = [engine.idem_write(marg, ext, r.k, r.start, r.n_own) for r in runners if r.n_own > 0]
+        return torch.cat(outs, dim=0)
     ys, extras = [], []
     for r in runners:
         x_ext = a[r.start:r.end + r.halo]

@@ -73,5 +73,49 @@ class OracleEngine:
             out = comb(out, tail.numpy()[..., None])
         return torch.from_numpy(np.ascontiguousarray(out))
 
+    # the per-axis marginal form for max (sharded.CudaEngine.idem_*): the
+    # rank's marginals of its planes, then its output planes from the global ones
+    def idem_ok(self, ext):
+        return self.op == "max" and self.dtype_name == "int64" and len(ext) >= 2 and sum(ext) <= 4096
+
+    def idem_marginals(self, x_own, ext, x0):
+        a = x_own.contiguous().numpy()
+        ident = np.iinfo(np.int64).min
+        parts = []
+        for ax, n in enumerate(ext):
+            m = np.full(n, ident, dtype=np.int64)
+            if a.size:
+                red = a.max(axis=tuple(i for i in range(a.ndim) if i != ax))
+                if ax == 0:
+                    m[x0:x0 + a.shape[0]] = red
+                else:
+                    m[:] = red
+            parts.append(m)
+        return torch.from_numpy(np.concatenate(parts))
+
+    def idem_write(self, marg, ext, box, x0, n_own):
+        m = marg.numpy()
+        ident = np.iinfo(np.int64).min
+        out = None
+        off = 0
+        for ax, n in enumerate(ext):
+            k = min(box[ax], n)
+            M = m[off:off + n]
+            off += n
+            P = np.maximum.accumulate(M)
+            S = np.maximum.accumulate(M[::-1])[::-1]
+            F = np.full(n, ident, dtype=np.int64)
+            F[1:] = P[:-1]
+            if k < n:
+                F[: n - k] = np.maximum(F[: n - k], S[k:])
+            if ax == 0:
+                F = F[x0:x0 + n_own]
+            shape = [1] * len(ext)
+            shape[ax] = F.shape[0]
+            Fb = F.reshape(shape)
+            out = Fb if out is None else np.maximum(out, Fb)
+        full = np.broadcast_to(out, (n_own,) + tuple(ext[1:]))
+        return torch.from_numpy(np.ascontiguousarray(full))
+
     def box_complement(self, R, box):
         return torch.from_numpy(orc.box_complement_excluded(R.numpy(), tuple(box), self.op))

@@ -22,7 +22,28 @@ CASES = [
     ((45, 12, 32), (20, 4, 4), "add-f64", 2),    # k0 = 20: fallback pass into a temporary
     ((9, 30, 1024), (2, 16, 16), "add-f32", 4),  # fused kernels on the shard
     ((5, 8, 8), (8, 2, 2), "add-i64", 2),        # one empty rank
+    ((5, 8, 8), (8, 2, 2), "max-i64", 2),        # marginal form with an empty rank
+    ((33, 17, 66), (4, 5, 8), "max-i64", 4),     # marginal form, uneven slabs, odd rows
 ]
+
+
+def test_sharded_max_takes_the_marginal_form():
+    """Box-complement over max shards as per-axis marginals: no halo, an
+    all-reduce of sum(ext) values (csrc/idem_max.cu)."""
+    import torch
+
+    import paper_2106_00124_b200 as ex
+    from paper_2106_00124_b200.sharded import CudaEngine, ShardedRunner, run_loopback
+
+    ops = ex.IntMaxOps()
+    ext, box = (40, 24, 48), (8, 4, 8)
+    engine = CudaEngine(ops, torch.device("cuda"))
+    r = ShardedRunner("box-complement", ops, ext, box, 1, 3, torch.device("cuda"),
+                      comm=object(), engine=engine)
+    assert r.idem
+    a = np.random.default_rng(1).integers(-2**40, 2**40, size=ext, dtype=np.int64)
+    got = run_loopback("box-complement", ops, torch.from_numpy(a).cuda(), box, 3, engine)
+    assert np.array_equal(got.cpu().numpy(), orc.box_complement_excluded(a, box, "max"))
 
 
 @pytest.mark.parametrize("ext,box,mono,world", CASES, ids=lambda v: str(v))

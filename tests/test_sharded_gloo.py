@@ -25,6 +25,7 @@ CASES = [
     ((16, 9), (5, 3), "box-complement", "max", np.int64),
     ((16, 9), (5, 3), "bdbs", "max", np.int64),
     ((5, 3, 4), (8, 2, 2), "box-complement", "add", np.int64),   # one rank empty
+    ((5, 3, 4), (8, 2, 2), "box-complement", "max", np.int64),   # marginal form, one rank empty
     ((20, 4, 6), (3, 2, 3), "bdbs", "add", np.float64),          # bit-exact float BDBS
     ((20, 4, 6), (3, 2, 3), "bdbsc", "add", np.float64),
     ((20, 4, 6), (3, 2, 3), "box-complement", "add", np.float32),
