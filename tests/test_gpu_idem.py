@@ -33,6 +33,10 @@ CASES = [
     ((4, 5, 6, 7, 8), (2, 2, 3, 3, 4)),
     ((1000, 1000), (32, 32)),
     ((2, 3000), (1, 100)),
+    ((50, 40, 1), (3, 4, 1)),          # a one-element last axis
+    ((1, 1, 300), (1, 1, 9)),          # only the last axis varies
+    ((7, 1, 5, 1, 9), (2, 1, 3, 1, 4)),
+    ((4000, 3, 2), (17, 2, 1)),        # many short rows
 ]
 
 
