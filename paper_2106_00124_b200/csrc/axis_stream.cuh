@@ -16,7 +16,10 @@
 //            row of the unit, a 16-value warp butterfly (17 shuffles) folds
 //            those across the warp's 128 columns, one partial per (row,
 //            128-column segment) -- no CTA barrier (a shared-memory fold
-//            needed two per unit and ran at 1.96 ms vs 1.42 ms on C4);
+//            needed two per unit and ran at 1.96 ms vs 1.42 ms on C4).  The
+//            butterfly of unit u+1 runs on its raw registers during unit u
+//            (AS_FOLD_NEXT), so its shuffle latency overlaps the block
+//            compute: C4 pass 1.426 -> 1.403 ms;
 //   EX == 2: the BDBSC total, folded per thread from registers.
 #pragma once
 
@@ -131,7 +134,10 @@ k_axis_stream(const T* __restrict__ in, T* __restrict__ out, int64_t outer, int6
     for (int64_t u = u0; u < u_end; ++u) {
       const int64_t us = u * U;
       const int rows_u = len;
-      {
+#ifndef AS_FOLD_NEXT
+#define AS_FOLD_NEXT 1
+#endif
+      if (!AS_FOLD_NEXT || u == u0) {
         const int64_t inseg = xe - us;
         fold_rows(cur, us, (int)(rows_u < inseg ? rows_u : inseg));
       }
@@ -153,6 +159,13 @@ k_axis_stream(const T* __restrict__ in, T* __restrict__ out, int64_t outer, int6
           if (r < nlen_u) nxt[r] = *reinterpret_cast<const VT*>(sn + r * N2);
       }
       issue(u + 3);
+      if (AS_FOLD_NEXT && u + 1 < u_end) {
+        // the next unit's row partials now, from its raw registers: the
+        // butterfly's shuffle latency overlaps this unit's block compute
+        const int64_t usn = us + U;
+        const int64_t inseg = xe - usn;
+        fold_rows(nxt, usn, (int)(nlen_u < inseg ? nlen_u : inseg));
+      }
 #pragma unroll
       for (int jb = 0; jb < G; ++jb) {
         const int64_t bs = us + (int64_t)jb * K1;
