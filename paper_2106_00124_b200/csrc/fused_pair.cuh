@@ -48,6 +48,15 @@ namespace exsum {
 #ifndef FP_NARROW_C
 #define FP_NARROW_C 8
 #endif
+// the stores of unit u's rows run inside unit u+1's axis-(d-2) pass, each row
+// right before its stage slot is rewritten (interleaving the streaming stores
+// with the compute instead of a store-only loop after the row op).  Measured
+// per mode: the box-complement row rounds gain (C4 f32 BLK 1.414 -> 1.322 ms,
+// C5 f64 -30 us, C4 4^3 -45 us), ROW_WIN loses (C4 BDBS 1.335 -> 1.408 ms:
+// its short row op leaves the store loop nothing to hide behind)
+#ifndef FP_DEFER_STORE
+#define FP_DEFER_STORE 1  // 1: the row-round modes (not ROW_WIN); 2: every mode
+#endif
 // Rows per streaming unit: 16 (a multiple of K1) for wide rows; narrow rows
 // (C <= 8: 64-thread CTAs whose shared ring and stage bound the CTAs per SM)
 // take 8-row units where K1 allows, doubling the resident CTAs.
@@ -180,6 +189,19 @@ k_fused_pair(const T* __restrict__ in, T* __restrict__ out, int64_t outer, int64
       if (r < len) cur[r] = *reinterpret_cast<const CT*>(raw + col + r * RAWP);
     issue(u0 + 2);
 
+    constexpr bool DEFER = !STRIP && (FP_DEFER_STORE == 2 || (FP_DEFER_STORE == 1 && MODE != ROW_WIN));
+    int prev_rows = 0;     // rows of the previous unit still in the stage (DEFER)
+    int64_t prev_us = 0;
+    // write row `r` of this unit's axis-(d-2) result to the stage; DEFER first
+    // stores the previous unit's row r from that slot
+    auto stage_put = [&](int r, const CT& v) {
+      if constexpr (DEFER) {
+        if (r < prev_rows)
+          st_stream<T, TV>(dst + (prev_us + r) * rs, *reinterpret_cast<const CT*>(wst + r * ROWP + pcol));
+      }
+      if (colthr) *reinterpret_cast<CT*>(wst + r * ROWP + pcol) = v;
+    };
+
     for (int64_t u = u0; u < u_end; ++u) {
       const int64_t us = u * U;
       const int rows_u = len;
@@ -227,12 +249,12 @@ k_fused_pair(const T* __restrict__ in, T* __restrict__ out, int64_t outer, int64
           if (bs == last_bs) {  // last block of axis d-2: W = S
 #pragma unroll
             for (int r = 0; r < K1; ++r)
-              if (r < blen && colthr) *reinterpret_cast<CT*>(wst + (jb * K1 + r) * ROWP + pcol) = cur[jb * K1 + r];
+              if (r < blen) stage_put(jb * K1 + r, cur[jb * K1 + r]);
           } else {
             // stitch with the next block's left-nested prefix (raw)
             const int64_t nrows = n1 - bs - K1;
             const int nlen = (int)(nrows < K1 ? nrows : K1);
-            if (colthr) *reinterpret_cast<CT*>(wst + (jb * K1) * ROWP + pcol) = cur[jb * K1];
+            stage_put(jb * K1, cur[jb * K1]);
             const int nb0 = jb + 1 < G ? (jb + 1) * K1 : 0;  // in range for the dead branch
             CT P = jb + 1 < G ? cur[nb0] : nxt[0];
 #pragma unroll
@@ -246,10 +268,15 @@ k_fused_pair(const T* __restrict__ in, T* __restrict__ out, int64_t outer, int64
               CT w;
 #pragma unroll
               for (int j = 0; j < TV; ++j) w.v[j] = Op::apply(cur[jb * K1 + r].v[j], P.v[j]);
-              if (colthr) *reinterpret_cast<CT*>(wst + (jb * K1 + r) * ROWP + pcol) = w;
+              stage_put(jb * K1 + r, w);
             }
           }
         }
+      }
+      if constexpr (DEFER) {
+        // rows of the previous unit this (shorter) unit did not overwrite
+        for (int r = rows_u; r < prev_rows; ++r)
+          st_stream<T, TV>(dst + (prev_us + r) * rs, *reinterpret_cast<const CT*>(wst + r * ROWP + pcol));
       }
       len = nlen_u;
       if constexpr (EARLY) {
@@ -553,9 +580,14 @@ k_fused_pair(const T* __restrict__ in, T* __restrict__ out, int64_t outer, int64
         __syncwarp();
       }
       __syncthreads();
-      if (!halo_thr)
-        for (int r = 0; r < rows_u; ++r)
-          st_stream<T, TV>(dst + (us + r) * rs, *reinterpret_cast<const CT*>(wst + r * ROWP + pcol));
+      if constexpr (DEFER) {
+        prev_rows = rows_u;
+        prev_us = us;
+      } else {
+        if (!halo_thr)
+          for (int r = 0; r < rows_u; ++r)
+            st_stream<T, TV>(dst + (us + r) * rs, *reinterpret_cast<const CT*>(wst + r * ROWP + pcol));
+      }
       if constexpr (!EARLY) {
         if (u + 1 < u_end) {
 #pragma unroll
@@ -564,6 +596,10 @@ k_fused_pair(const T* __restrict__ in, T* __restrict__ out, int64_t outer, int64
         }
         issue(u + 3);  // refills the slot unit u+1 just vacated
       }
+    }
+    if constexpr (DEFER) {
+      for (int r = 0; r < prev_rows; ++r)
+        st_stream<T, TV>(dst + (prev_us + r) * rs, *reinterpret_cast<const CT*>(wst + r * ROWP + pcol));
     }
     cp_async_wait<0>();
   }
