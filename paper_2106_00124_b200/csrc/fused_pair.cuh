@@ -51,11 +51,13 @@ namespace exsum {
 // the stores of unit u's rows run inside unit u+1's axis-(d-2) pass, each row
 // right before its stage slot is rewritten (interleaving the streaming stores
 // with the compute instead of a store-only loop after the row op).  Measured
-// per mode: the box-complement row rounds gain (C4 f32 BLK 1.414 -> 1.322 ms,
-// C5 f64 -30 us, C4 4^3 -45 us), ROW_WIN loses (C4 BDBS 1.335 -> 1.408 ms:
-// its short row op leaves the store loop nothing to hide behind)
+// per mode and shape: the box-complement row rounds gain everywhere (C4 f32
+// BLK 1.414 -> 1.322 ms, C5 f64 -30 us, C4 4^3 -45 us), ROW_WIN gains on
+// 8-byte rows (C5 f64 box 8^3 / 16^3 -25 us), narrow float32 rows and k = 4
+// (C4 box 4^3 -36 us) but loses on 1024-wide float32 rows with k >= 8 (C4 BDBS
+// 1.335 -> 1.408 ms): those keep the store loop after the row op (WIN_SLOW)
 #ifndef FP_DEFER_STORE
-#define FP_DEFER_STORE 1  // 1: the row-round modes (not ROW_WIN); 2: every mode
+#define FP_DEFER_STORE 1  // 1: every mode but WIN_SLOW below; 2: every mode
 #endif
 // Rows per streaming unit: 16 (a multiple of K1) for wide rows; narrow rows
 // (C <= 8: 64-thread CTAs whose shared ring and stage bound the CTAs per SM)
@@ -189,7 +191,8 @@ k_fused_pair(const T* __restrict__ in, T* __restrict__ out, int64_t outer, int64
       if (r < len) cur[r] = *reinterpret_cast<const CT*>(raw + col + r * RAWP);
     issue(u0 + 2);
 
-    constexpr bool DEFER = !STRIP && (FP_DEFER_STORE == 2 || (FP_DEFER_STORE == 1 && MODE != ROW_WIN));
+    constexpr bool WIN_SLOW = MODE == ROW_WIN && sizeof(T) == 4 && C == 32 && K1 >= 8;
+    constexpr bool DEFER = !STRIP && (FP_DEFER_STORE == 2 || (FP_DEFER_STORE == 1 && !WIN_SLOW));
     int prev_rows = 0;     // rows of the previous unit still in the stage (DEFER)
     int64_t prev_us = 0;
     // write row `r` of this unit's axis-(d-2) result to the stage; DEFER first

@@ -25,7 +25,7 @@ from paper_2106_00124_b200 import _native
 cfg, route, op, reps = %(cfg)r, %(route)r, %(op)r, %(reps)d
 ext, dtype, box, _, _ = bench.CONFIGS[cfg]
 if %(box)r: box = tuple(%(box)r)
-x = bench.make_input(cfg, "cuda")
+x = bench.make_input(cfg, "cuda", shape=tuple(%(shape)r) or None)
 ops = {("int64","max"): ex.IntMaxOps(), ("int64","add"): ex.IntAddOps(), ("float32","add"): ex.Float32AddOps(),
        ("float64","add"): ex.FloatAddOps()}[(dtype, op)]
 fn = {"bdbs": ex.bdbs_included, "bdbsc": ex.bdbs_excluded, "box-complement": ex.box_complement_excluded}[route]
@@ -65,6 +65,7 @@ def main():
     ap.add_argument("--op", default="max")
     ap.add_argument("--box", default="")
     ap.add_argument("--reps", type=int, default=20)
+    ap.add_argument("--shape", default="", help="extents instead of the config's (same dtype)")
     ap.add_argument("libs", nargs="*")
     args = ap.parse_args()
     box = [int(v) for v in args.box.split(",")] if args.box else []
@@ -73,8 +74,9 @@ def main():
         env = dict(os.environ)
         if lib != "default":
             env["EXSUM_LIB"] = os.path.abspath(lib)
+        shape = [int(v) for v in args.shape.split(",")] if args.shape else []
         code = CHILD % {"root": ROOT, "cfg": args.config, "route": args.route, "op": args.op,
-                        "reps": args.reps, "box": box}
+                        "reps": args.reps, "box": box, "shape": shape}
         r = subprocess.run([sys.executable, "-c", code], env=env, capture_output=True, text=True)
         line = r.stdout.strip().splitlines()[-1] if r.stdout.strip() else r.stderr[-500:]
         print(os.path.basename(lib), line, flush=True)
