@@ -30,6 +30,13 @@
 
 namespace exsum {
 
+#ifndef AS_RING
+#define AS_RING 2  // shared-memory ring slots (units in flight beyond the two in registers)
+#endif
+#ifndef AS_ABL
+#define AS_ABL 0  // measurement only: 1 skips the row-partial stores, 2 the whole fold
+#endif
+
 template <class T, class Op, int C, int K1, int EX>
 __global__ void __launch_bounds__(32 * C / (16 / sizeof(T)), 1)
 k_axis_stream(const T* __restrict__ in, T* __restrict__ out, int64_t outer, int64_t n1,
@@ -45,7 +52,7 @@ k_axis_stream(const T* __restrict__ in, T* __restrict__ out, int64_t outer, int6
   constexpr int U = G * K1;                      // rows per unit
   typedef Vec<T, VE> VT;
   extern __shared__ __align__(16) unsigned char smem[];
-  T* raw = reinterpret_cast<T*>(smem);  // [2][U][N2]
+  T* raw = reinterpret_cast<T*>(smem);  // [AS_RING][U][N2]
   const int tid = threadIdx.x;
   const int lane = tid & 31;
   const int warp = tid >> 5;
@@ -71,6 +78,19 @@ k_axis_stream(const T* __restrict__ in, T* __restrict__ out, int64_t outer, int6
     const int64_t u_end = (xe + U - 1) / U;
     const T* src = in + o * n1 * inner + strip * N2 + col;
     T* dst = out + o * nout * inner + strip * N2 + col;
+    // EX == 1: where this warp's row partials go -- rowpart[row][seg] with
+    // row = (o * nout + x) * rpi + cq / row_len, seg = (cq % row_len) / 128
+    // (inner is a multiple of row_len): a row's partials are contiguous, so the
+    // CTA's warps fill whole lines together (a [seg][row] layout scattered them
+    // over row_len / 128 regions: C4 pass 1.409 -> see DESIGN); the divisions
+    // once per item, not per unit
+    int64_t rp_base = 0, rp_step = 0;
+    if constexpr (EX == 1) {
+      const int64_t cq = strip * N2 + warp * (32 * VE);
+      const int64_t ppr = row_len / (32 * VE);
+      rp_step = (inner / row_len) * ppr;
+      rp_base = (o * nout * (inner / row_len) + cq / row_len) * ppr + (cq % row_len) / (32 * VE);
+    }
 
     auto rows_of = [&](int64_t ui) -> int {
       const int64_t avail = n1 - ui * U;
@@ -79,7 +99,7 @@ k_axis_stream(const T* __restrict__ in, T* __restrict__ out, int64_t outer, int6
     };
     auto issue = [&](int64_t ui) {
       const int rows = rows_of(ui);
-      T* d = raw + ((ui - u0) & 1) * (U * N2) + col;
+      T* d = raw + ((ui - u0) % AS_RING) * (U * N2) + col;
       for (int r = 0; r < rows; ++r) cp_async16(d + r * N2, src + (ui * U + r) * inner);
       cp_async_commit();
     };
@@ -88,7 +108,7 @@ k_axis_stream(const T* __restrict__ in, T* __restrict__ out, int64_t outer, int6
     // shuffles for 16 rows; lanes whose low bits are zero store one partial
     // per (row, 128-column segment) to rowpart[segment][row].
     auto fold_rows = [&](const VT (&blk)[U], int64_t x0, int nrows) {
-      if constexpr (EX == 1) {
+      if constexpr (EX == 1 && AS_ABL != 2) {
         T sv[U];
 #pragma unroll
         for (int r = 0; r < U; ++r) {
@@ -114,22 +134,22 @@ k_axis_stream(const T* __restrict__ in, T* __restrict__ out, int64_t outer, int6
 #pragma unroll
         for (int off = LOWB >> 1; off >= 1; off >>= 1)
           sv[0] = Op::apply(sv[0], __shfl_xor_sync(0xffffffffu, sv[0], off));
+        if (AS_ABL == 1 && sv[0] != T(-12345.678)) return;
         if ((lane & (LOWB - 1)) == 0 && rowbase < nrows) {
-          const int64_t e = (o * nout + x0 + rowbase) * inner + strip * N2 + warp * (32 * VE);
-          rowpart[((e % row_len) / (32 * VE)) * rows_total + e / row_len] = sv[0];
+          rowpart[rp_base + (x0 + rowbase) * rp_step] = sv[0];
         }
       }
     };
 
-    issue(u0);
-    issue(u0 + 1);
-    cp_async_wait<1>();
+#pragma unroll
+    for (int i = 0; i < AS_RING; ++i) issue(u0 + i);
+    cp_async_wait<AS_RING - 1>();
     VT cur[U];
     int len = rows_of(u0);
 #pragma unroll
     for (int r = 0; r < U; ++r)
       if (r < len) cur[r] = *reinterpret_cast<const VT*>(raw + col + r * N2);
-    issue(u0 + 2);
+    issue(u0 + AS_RING);
 
     for (int64_t u = u0; u < u_end; ++u) {
       const int64_t us = u * U;
@@ -150,15 +170,15 @@ k_axis_stream(const T* __restrict__ in, T* __restrict__ out, int64_t outer, int6
           }
       }
       const int nlen_u = rows_of(u + 1);
-      const T* sn = raw + ((u + 1 - u0) & 1) * (U * N2) + col;
+      const T* sn = raw + ((u + 1 - u0) % AS_RING) * (U * N2) + col;
       VT nxt[U];
       if (nlen_u > 0) {
-        cp_async_wait<1>();  // unit u+1 has landed (u+2 may still be in flight)
+        cp_async_wait<AS_RING - 1>();  // unit u+1 has landed (u+2.. may still be in flight)
 #pragma unroll
         for (int r = 0; r < U; ++r)
           if (r < nlen_u) nxt[r] = *reinterpret_cast<const VT*>(sn + r * N2);
       }
-      issue(u + 3);
+      issue(u + AS_RING + 1);
       if (AS_FOLD_NEXT && u + 1 < u_end) {
         // the next unit's row partials now, from its raw registers: the
         // butterfly's shuffle latency overlaps this unit's block compute
@@ -248,7 +268,7 @@ int go_axis_stream_c(const T* in, T* out, int64_t outer, int64_t n, int64_t inne
   constexpr int N2 = 32 * C;
   constexpr int NT = N2 / VE;
   constexpr int U = (16 / K1) * K1;
-  const size_t smem = (size_t)2 * U * N2 * sizeof(T);
+  const size_t smem = (size_t)AS_RING * U * N2 * sizeof(T);
   int per_sm = (int)((228 * 1024) / (smem + 1024));
   if (per_sm > 2048 / NT) per_sm = 2048 / NT;
   if (per_sm < 1) per_sm = 1;

@@ -59,7 +59,7 @@ int launch_complement(int dtype, const void* in, void* out, int64_t N, const voi
                       cudaStream_t s);
 
 // Box-complement tail of a 3-D array (tail2d.cu): R (n0 x n1) from row
-// partials part[ppr][n0*n1] (or, part == nullptr, R as given), R2 (n0) its
+// partials part[n0*n1][ppr] (or, part == nullptr, R as given), R2 (n0) its
 // fold over the last axis, Tout = BC(R, (k0, k1)).  stage 0 writes R and R2,
 // stage 1 (after it) writes Tout; one launch each.
 int tail2d_ok(int dtype, int64_t n0, int64_t n1, int64_t k0);

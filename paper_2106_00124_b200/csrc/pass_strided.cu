@@ -86,8 +86,7 @@ k_strided_reg(const T* __restrict__ in, T* __restrict__ out, int64_t outer, int6
       if ((lane & (LOWB - 1)) == 0 && rowbase < nrows) {
         const int64_t c0 = c - lane;  // the warp's first column vector
         const int64_t e = (o * n + x0 + rowbase) * inner + c0 * V;
-        const int64_t rows_total = outer * nout * inner / row_len;
-        rowpart[((e % row_len) / (32 * V)) * rows_total + e / row_len] = sv[0];
+        rowpart[(e / row_len) * (row_len / (32 * V)) + (e % row_len) / (32 * V)] = sv[0];
       }
     } else if constexpr (EXTRA == 2) {
 #pragma unroll

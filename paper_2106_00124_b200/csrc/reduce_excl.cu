@@ -334,14 +334,14 @@ int go_excl(const T* W, T* out, const T* Tail, int64_t rows, int64_t n, int64_t 
 
 int reduce_partials_count() { return kPartialsCap; }
 
-// part is [ppr][rows] (written by k_strided_reg<..., EXTRA=1>)
+// part is [rows][ppr] (written by k_axis_stream<EX=1> / k_strided_reg<..., EXTRA=1>)
 template <class T, class Op>
 __global__ void k_rowpart_final(const T* __restrict__ part, T* __restrict__ R, int64_t rows,
                                 int64_t ppr) {
   for (int64_t r = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; r < rows;
        r += (int64_t)gridDim.x * blockDim.x) {
-    T acc = part[r];
-    for (int64_t i = 1; i < ppr; ++i) acc = Op::apply(acc, part[i * rows + r]);
+    T acc = part[r * ppr];
+    for (int64_t i = 1; i < ppr; ++i) acc = Op::apply(acc, part[r * ppr + i]);
     R[r] = acc;
   }
 }

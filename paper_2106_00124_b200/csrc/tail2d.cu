@@ -51,53 +51,52 @@ __device__ __forceinline__ T block_fold(T v, T* sh) {
   return t;
 }
 
-// part: [ppr][n0 * n1] row partials (ppr > 0) or nullptr (R already holds R).
-// A CTA per x0 row of R; every thread owns PPT consecutive columns and issues
-// all of its partial loads before folding them (up to 16 partials per row in
-// registers, 8 at a time: the axis-0 pass leaves row_len / (32 * 16 B) of them).
+// part: [n0 * n1][ppr] row partials (ppr > 0) or nullptr (R already holds R).
+// A CTA per x0 row of R, a thread per element of it: its ppr partials are
+// contiguous, read as 16-byte vectors (consecutive threads on consecutive
+// rows: the warp's loads cover one contiguous span), folded in order.
 template <class T, class Op>
 __global__ void __launch_bounds__(kTailThreads)
 k_tail_rows(const T* __restrict__ part, int64_t ppr, T* __restrict__ R, T* __restrict__ R2,
             int64_t n0, int64_t n1) {
   __shared__ T sh[kTailWarps];
-  constexpr int PPT = 16 / sizeof(T);  // columns per thread per step (16 bytes)
-  constexpr int PMAX = 8;
-  const int64_t rows = n0 * n1;
+  constexpr int VE = 16 / sizeof(T);
+  constexpr int PMAX = 16;  // partials per batch of loads
   for (int64_t x0 = blockIdx.x; x0 < n0; x0 += gridDim.x) {
     T acc = Op::template identity<T>();
-    for (int64_t c0 = (int64_t)threadIdx.x * PPT; c0 < n1; c0 += (int64_t)blockDim.x * PPT) {
-      const int64_t r0 = x0 * n1 + c0;
-      const int cn = (int)(n1 - c0 < PPT ? n1 - c0 : PPT);
-      T v[PPT];
+    for (int64_t c = threadIdx.x; c < n1; c += blockDim.x) {
+      const int64_t r = x0 * n1 + c;
+      T v;
       if (part) {
+        const T* pp = part + r * ppr;
+        const bool vec = ppr % VE == 0;  // then every row's span is 16-byte aligned
         for (int64_t i0 = 0; i0 < ppr; i0 += PMAX) {
-          T q[PMAX][PPT];
+          T q[PMAX];
+          const int cnt = (int)(ppr - i0 < PMAX ? ppr - i0 : PMAX);
+          if (vec) {
 #pragma unroll
-          for (int i = 0; i < PMAX; ++i)
+            for (int w = 0; w < PMAX / VE; ++w)
+              if (w * VE < cnt) {
+                const Vec<T, VE> t = *reinterpret_cast<const Vec<T, VE>*>(pp + i0 + w * VE);
 #pragma unroll
-            for (int j = 0; j < PPT; ++j)
-              if (i0 + i < ppr && j < cn) q[i][j] = part[(i0 + i) * rows + r0 + j];
+                for (int e = 0; e < VE; ++e) q[w * VE + e] = t.v[e];
+              }
+          } else {
 #pragma unroll
-          for (int j = 0; j < PPT; ++j) {
-            if (j >= cn) continue;
-            T t = i0 == 0 ? q[0][j] : Op::apply(v[j], q[0][j]);
-#pragma unroll
-            for (int i = 1; i < PMAX; ++i)
-              if (i0 + i < ppr) t = Op::apply(t, q[i][j]);
-            v[j] = t;
+            for (int i = 0; i < PMAX; ++i)
+              if (i < cnt) q[i] = pp[i0 + i];
           }
+          T t = i0 == 0 ? q[0] : Op::apply(v, q[0]);
+#pragma unroll
+          for (int i = 1; i < PMAX; ++i)
+            if (i < cnt) t = Op::apply(t, q[i]);
+          v = t;
         }
-#pragma unroll
-        for (int j = 0; j < PPT; ++j)
-          if (j < cn) R[r0 + j] = v[j];
+        R[r] = v;
       } else {
-#pragma unroll
-        for (int j = 0; j < PPT; ++j)
-          if (j < cn) v[j] = R[r0 + j];
+        v = R[r];
       }
-#pragma unroll
-      for (int j = 0; j < PPT; ++j)
-        if (j < cn) acc = Op::apply(acc, v[j]);
+      acc = Op::apply(acc, v);
     }
     acc = block_fold<T, Op>(acc, sh);
     if (threadIdx.x == 0) R2[x0] = acc;
