@@ -296,10 +296,16 @@ k_rows_tile(const T* __restrict__ in, T* __restrict__ out, int64_t rows, int64_t
   static_assert(CMAX % K == 0 && CMAX % VE == 0, "chunk shape");
   static_assert(CVMAX <= 32, "the multiply-shift division below is exact for CV <= 32");
   typedef Vec<T, VE> VT;
-  __shared__ __align__(16) T smem[WARPS][33 * (CMAX + 2 * VE)];
+  // wide chunks (CVMAX > 8, e.g. f64 k = 32) would hold two chunks of
+  // registers at once to prefetch: they double-buffer the stage instead, the
+  // next tile's 16-byte cp.async copies in flight while this one is computed
+  constexpr bool PREFETCH = CVMAX <= 8;
+  constexpr int SLOT = 33 * (CMAX + 2 * VE);  // one staged tile, padded chunks
+  extern __shared__ __align__(16) unsigned char smem_raw[];
   const int lane = threadIdx.x & 31;
   const int wib = threadIdx.x >> 5;
-  T* sm = smem[wib];
+  T* smw = reinterpret_cast<T*>(smem_raw) + wib * (PREFETCH ? 1 : 2) * SLOT;
+  T* sm = smw;
   const int64_t warp = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
   const int64_t nwarps = ((int64_t)gridDim.x * blockDim.x) >> 5;
   const T tot = total ? (T)(*total) : T(0);
@@ -309,13 +315,11 @@ k_rows_tile(const T* __restrict__ in, T* __restrict__ out, int64_t rows, int64_t
   const int64_t ntiles = (nchunks + 31) / 32;
 
   // each lane's share of a tile's 16-byte vectors, held in registers so the
-  // next tile's loads are in flight while this one is computed
+  // next tile's loads are in flight while this one is computed (PREFETCH)
   constexpr int PV = (33 * CVMAX + 31) / 32;
-  // wide chunks (CVMAX > 8, e.g. f64 k = 32) would hold two chunks of
-  // registers at once: they load each tile right before staging it instead
-  constexpr bool PREFETCH = CVMAX <= 8;
-  VT pre[PV];
+  VT pre[PREFETCH ? PV : 1];
   auto load_tile = [&](int64_t t) {
+    if constexpr (!PREFETCH) return;
     if (t >= ntiles) return;
     const int64_t a0 = nchunks - t * 32;
     const int nl = a0 >= 33 ? 33 : (int)a0;
@@ -326,23 +330,45 @@ k_rows_tile(const T* __restrict__ in, T* __restrict__ out, int64_t rows, int64_t
       if (v < nl * CV) pre[i] = ld_stream<T, VE>(reinterpret_cast<const T*>(src + v));
     }
   };
+  // !PREFETCH: the tile's vectors straight into stage slot `slot` by cp.async
+  auto copy_tile = [&](int64_t t, int slot) {
+    if (t < ntiles) {
+      const int64_t a0 = nchunks - t * 32;
+      const int nl = a0 >= 33 ? 33 : (int)a0;
+      const VT* src = reinterpret_cast<const VT*>(in + t * 32 * C);
+      T* dstm = smw + slot * SLOT;
+      for (int v = lane; v < nl * CV; v += 32) {
+        const int cq = (int)(((unsigned)v * cv_magic) >> 16);  // v / CV
+        cp_async16(dstm + cq * STRIDE + (v - cq * CV) * VE, src + v);
+      }
+    }
+    cp_async_commit();
+  };
   if (PREFETCH) load_tile(warp);
+  else copy_tile(warp, 0);
+  int slot = 0;
 
   for (int64_t tile = warp; tile < ntiles; tile += nwarps) {
     const int64_t c0 = tile * 32;
     const int64_t avail = nchunks - c0;  // chunks left from c0 (>= 1)
     const int nload = avail >= 33 ? 33 : (int)avail;
-    if (!PREFETCH) load_tile(tile);
+    if constexpr (PREFETCH) {
 #pragma unroll
-    for (int i = 0; i < PV; ++i) {
-      const int v = lane + 32 * i;
-      if (v < nload * CV) {
-        const int cq = (int)(((unsigned)v * cv_magic) >> 16);  // v / CV (v < 4096)
-        *reinterpret_cast<VT*>(sm + cq * STRIDE + (v - cq * CV) * VE) = pre[i];
+      for (int i = 0; i < PV; ++i) {
+        const int v = lane + 32 * i;
+        if (v < nload * CV) {
+          const int cq = (int)(((unsigned)v * cv_magic) >> 16);  // v / CV (v < 4096)
+          *reinterpret_cast<VT*>(sm + cq * STRIDE + (v - cq * CV) * VE) = pre[i];
+        }
       }
+      __syncwarp();
+      load_tile(tile + nwarps);
+    } else {
+      sm = smw + slot * SLOT;
+      copy_tile(tile + nwarps, slot ^ 1);  // the slot the previous tile left
+      cp_async_wait<1>();                  // this tile's copies have landed
+      __syncwarp();
     }
-    __syncwarp();
-    if (PREFETCH) load_tile(tile + nwarps);
     const int64_t c = c0 + lane;
     const bool valid = lane < nload && lane < 32 && c < nchunks;
     const int64_t xc = valid ? (c % cpr) * C : 0;  // chunk start within its row
@@ -398,7 +424,9 @@ k_rows_tile(const T* __restrict__ in, T* __restrict__ out, int64_t rows, int64_t
                        *reinterpret_cast<const VT*>(sm + (((unsigned)v * cv_magic) >> 16) * STRIDE +
                                                     (v - (int)(((unsigned)v * cv_magic) >> 16) * CV) * VE));
     __syncwarp();
+    slot ^= 1;
   }
+  if constexpr (!PREFETCH) cp_async_wait<0>();
 }
 
 // ---------------------------------------------- k == n > 32: whole-row suffix --
@@ -480,8 +508,12 @@ int go_tile(const T* in, T* out, int64_t rows, int64_t n, const typename AccOf<T
   const int64_t cap = (int64_t)num_sms() * 16;
   if (grid > cap) grid = cap;
   if (grid < 1) grid = 1;
-  k_rows_tile<T, Op, K, C, WARPS, RT><<<(unsigned)grid, WARPS * 32, 0, s>>>(in, out, rows, n,
-                                                                           total, c_rt);
+  constexpr int VE = 16 / (int)sizeof(T);
+  constexpr bool PREFETCH = C / VE <= 8;
+  const size_t smem = (size_t)WARPS * (PREFETCH ? 1 : 2) * 33 * (C + 2 * VE) * sizeof(T);
+  ensure_smem((const void*)k_rows_tile<T, Op, K, C, WARPS, RT>, smem);
+  k_rows_tile<T, Op, K, C, WARPS, RT><<<(unsigned)grid, WARPS * 32, smem, s>>>(in, out, rows, n,
+                                                                              total, c_rt);
   return 1;
 }
 
