@@ -458,8 +458,13 @@ k_rows_suffix(const T* __restrict__ in, T* __restrict__ out, int64_t rows, int64
     {
       const int64_t xs = n - W > 0 ? n - W : 0;
       const int64_t x = xs + lane;
+      if (nr == 32 && x < n) {  // unpredicated: all 32 loads in flight at once
 #pragma unroll
-      for (int r = 0; r < 32; ++r) v[r] = (r < nr && x < n) ? ld1(in + (r0 + r) * n + x) : T(0);
+        for (int r = 0; r < 32; ++r) v[r] = ld1(in + (r0 + r) * n + x);
+      } else {
+#pragma unroll
+        for (int r = 0; r < 32; ++r) v[r] = (r < nr && x < n) ? ld1(in + (r0 + r) * n + x) : T(0);
+      }
     }
     T S = T(0);
     for (int64_t xe = n; xe > 0; xe -= W) {
@@ -471,8 +476,13 @@ k_rows_suffix(const T* __restrict__ in, T* __restrict__ out, int64_t rows, int64
       if (xs > 0) {
         const int64_t ns = xs - W > 0 ? xs - W : 0;
         const int64_t x = ns + lane;
+        if (nr == 32 && x < xs) {
 #pragma unroll
-        for (int r = 0; r < 32; ++r) v[r] = (r < nr && x < xs) ? ld1(in + (r0 + r) * n + x) : T(0);
+          for (int r = 0; r < 32; ++r) v[r] = ld1(in + (r0 + r) * n + x);
+        } else {
+#pragma unroll
+          for (int r = 0; r < 32; ++r) v[r] = (r < nr && x < xs) ? ld1(in + (r0 + r) * n + x) : T(0);
+        }
       }
       if (lane < nr) {
         int x = w - 1;
