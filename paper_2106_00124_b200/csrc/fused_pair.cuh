@@ -192,14 +192,18 @@ k_fused_pair(const T* __restrict__ in, T* __restrict__ out, int64_t outer, int64
     issue(u0 + 2);
 
     constexpr bool WIN_SLOW = MODE == ROW_WIN && sizeof(T) == 4 && C == 32 && K1 >= 8;
-    constexpr bool DEFER = !STRIP && (FP_DEFER_STORE == 2 || (FP_DEFER_STORE == 1 && !WIN_SLOW));
+#ifndef FP_DEFER_STRIP
+#define FP_DEFER_STRIP 0
+#endif
+    constexpr bool DEFER = (!STRIP || FP_DEFER_STRIP) &&
+                           (FP_DEFER_STORE == 2 || (FP_DEFER_STORE == 1 && !WIN_SLOW));
     int prev_rows = 0;     // rows of the previous unit still in the stage (DEFER)
     int64_t prev_us = 0;
     // write row `r` of this unit's axis-(d-2) result to the stage; DEFER first
     // stores the previous unit's row r from that slot
     auto stage_put = [&](int r, const CT& v) {
       if constexpr (DEFER) {
-        if (r < prev_rows)
+        if (r < prev_rows && !halo_thr)
           st_stream<T, TV>(dst + (prev_us + r) * rs, *reinterpret_cast<const CT*>(wst + r * ROWP + pcol));
       }
       if (colthr) *reinterpret_cast<CT*>(wst + r * ROWP + pcol) = v;
@@ -278,7 +282,7 @@ k_fused_pair(const T* __restrict__ in, T* __restrict__ out, int64_t outer, int64
       }
       if constexpr (DEFER) {
         // rows of the previous unit this (shorter) unit did not overwrite
-        for (int r = rows_u; r < prev_rows; ++r)
+        for (int r = rows_u; r < (halo_thr ? 0 : prev_rows); ++r)
           st_stream<T, TV>(dst + (prev_us + r) * rs, *reinterpret_cast<const CT*>(wst + r * ROWP + pcol));
       }
       len = nlen_u;
@@ -601,7 +605,7 @@ k_fused_pair(const T* __restrict__ in, T* __restrict__ out, int64_t outer, int64
       }
     }
     if constexpr (DEFER) {
-      for (int r = 0; r < prev_rows; ++r)
+      for (int r = 0; r < (halo_thr ? 0 : prev_rows); ++r)
         st_stream<T, TV>(dst + (prev_us + r) * rs, *reinterpret_cast<const CT*>(wst + r * ROWP + pcol));
     }
     cp_async_wait<0>();
