@@ -36,6 +36,9 @@ namespace exsum {
 #ifndef AS_ABL
 #define AS_ABL 0  // measurement only: 1 skips the row-partial stores, 2 the whole fold
 #endif
+#ifndef AS_DEFER
+#define AS_DEFER 0  // 1: unit u's output rows leave during unit u+1 through a per-thread stage
+#endif
 
 template <class T, class Op, int C, int K1, int EX>
 __global__ void __launch_bounds__(32 * C / (16 / sizeof(T)), 1)
@@ -53,6 +56,9 @@ k_axis_stream(const T* __restrict__ in, T* __restrict__ out, int64_t outer, int6
   typedef Vec<T, VE> VT;
   extern __shared__ __align__(16) unsigned char smem[];
   T* raw = reinterpret_cast<T*>(smem);  // [AS_RING][U][N2]
+  // AS_DEFER: a stage of U output rows; each thread touches only its own
+  // column vector of it, so no barrier is needed
+  T* stg = raw + AS_RING * U * N2;      // [U][N2]
   const int tid = threadIdx.x;
   const int lane = tid & 31;
   const int warp = tid >> 5;
@@ -151,6 +157,13 @@ k_axis_stream(const T* __restrict__ in, T* __restrict__ out, int64_t outer, int6
       if (r < len) cur[r] = *reinterpret_cast<const VT*>(raw + col + r * N2);
     issue(u0 + AS_RING);
 
+    int prev_w = 0;        // AS_DEFER: stage rows [0, prev_w) still hold unit prev_us's output
+    int64_t prev_us = 0;
+    auto flush = [&](int from, int to) {
+      for (int r = from; r < to; ++r)
+        st_stream<T, VE>(dst + (prev_us + r) * inner, *reinterpret_cast<const VT*>(stg + r * N2 + col));
+    };
+
     for (int64_t u = u0; u < u_end; ++u) {
       const int64_t us = u * U;
       const int rows_u = len;
@@ -203,7 +216,14 @@ k_axis_stream(const T* __restrict__ in, T* __restrict__ out, int64_t outer, int6
 #pragma unroll
               for (int j = 0; j < VE; ++j) w.v[j] = OpAdd::inverse<T>(tot, w.v[j]);
             }
-            st_stream<T, VE>(dst + (bs + r) * inner, w);
+            if constexpr (AS_DEFER) {
+              const int slot = jb * K1 + r;
+              VT* sp = reinterpret_cast<VT*>(stg + slot * N2 + col);
+              if (slot < prev_w) st_stream<T, VE>(dst + (prev_us + slot) * inner, *sp);
+              *sp = w;
+            } else {
+              st_stream<T, VE>(dst + (bs + r) * inner, w);
+            }
           };
           if (bs == last_bs) {
 #pragma unroll
@@ -231,12 +251,21 @@ k_axis_stream(const T* __restrict__ in, T* __restrict__ out, int64_t outer, int6
           }
         }
       }
+      if constexpr (AS_DEFER) {
+        // this unit wrote stage rows [0, w): the rest of the previous unit's leave now
+        const int64_t wr = (xe - us < rows_u ? xe - us : rows_u);
+        const int w = (int)(wr > 0 ? wr : 0);
+        flush(w, prev_w);
+        prev_w = w;
+        prev_us = us;
+      }
       len = nlen_u;
       if (u + 1 < u_end) {
 #pragma unroll
         for (int r = 0; r < U; ++r) cur[r] = nxt[r];
       }
     }
+    if constexpr (AS_DEFER) flush(0, prev_w);
     cp_async_wait<0>();
     __syncthreads();  // the next item refills both slots
   }
@@ -268,7 +297,7 @@ int go_axis_stream_c(const T* in, T* out, int64_t outer, int64_t n, int64_t inne
   constexpr int N2 = 32 * C;
   constexpr int NT = N2 / VE;
   constexpr int U = (16 / K1) * K1;
-  const size_t smem = (size_t)AS_RING * U * N2 * sizeof(T);
+  const size_t smem = (size_t)(AS_RING + (AS_DEFER ? 1 : 0)) * U * N2 * sizeof(T);
   int per_sm = (int)((228 * 1024) / (smem + 1024));
   if (per_sm > 2048 / NT) per_sm = 2048 / NT;
   if (per_sm < 1) per_sm = 1;
