@@ -18,6 +18,10 @@
     on the band plus its k0 - 1 halo planes (the band's windows never see the
     sub-array's end), and BDBSC against float64 (total - BDBS) with the
     BDBSC contract (S = sum|A|).
+* C4 in full (round 2): every one of the 1024 planes of the box-complement
+  output against the float64 decomposition; BDBS bit-exact against the float32
+  oracle on the whole array; BDBSC on the whole array against float64
+  total - BDBS.
 * C1 (float64 1024^2 uniform [0,1), box 32^2): all three routes against the
   oracle at full size (BDBS bit-exact).
 * The C4 kernels on the default path (no EXSUM_* knobs) at (64, 96, 1024),
@@ -163,3 +167,96 @@ def test_c4_kernels_default_path(ex, route):
     want = orc.ROUTES[route](a.astype(np.float64), k, "add")
     ok, ratio, rel = compare(route, got, want, a, k, orc)
     assert ok, (route, ratio, rel)
+
+
+def test_c4_box_complement_every_plane(ex):
+    """The headline output checked in full: every one of the 1024 planes of the
+    C4 box-complement (bench.py's seeded input) against the float64 reference
+    decomposition (excluded.py:129-159 peeling axis 0, see the module
+    docstring), with the box-complement contract (S = BC(|A|) = the float64
+    answer, A >= 0).  Prefix planes P_y = sum_{y' < y} A stream in float64; the
+    suffix S_{x0+k0} = R1 - P_{x0+k0} (R1 the column sums) -- the checker's own
+    float64 subtraction is ~1e-16 relative, far inside the float32 bound."""
+    import collections
+
+    import torch
+
+    assert not os.environ.get("EXSUM_L2PIPE")
+    x = _bench_input("c4")
+    n0 = x.shape[0]
+    k = (16, 16, 16)
+    bc = ex.box_complement_excluded(ex.Tensor(ex.Float32AddOps(), x), k).data
+    xh = x.cpu().numpy()
+    del x
+    r1 = np.zeros(xh.shape[1:], np.float64)
+    for y in range(n0):
+        r1 += xh[y]
+    tail = orc.box_complement_excluded(r1, k[1:])
+    D = depth("box-complement", (n0,) + r1.shape, k)
+    tiny = np.finfo(np.float64).tiny
+    ring = collections.deque()  # (index y, P_y) for the last k0 + 1 prefixes
+    P = np.zeros(xh.shape[1:], np.float64)
+    worst = 0.0
+
+    def check(x0, p_x0, p_far):
+        nonlocal worst
+        s = p_x0 + (r1 - p_far) if p_far is not None else p_x0
+        want = orc.bdbs_included(s, k[1:]) + tail
+        got = bc[x0].cpu().numpy().astype(np.float64)
+        ratio = float(np.max(np.abs(got - want) / (D * 2.0**-24 * want + tiny)))
+        worst = max(worst, ratio)
+        assert ratio <= 1.0, (x0, ratio)
+
+    for y in range(n0 + 1):  # P holds P_y = sum of planes < y
+        ring.append((y, P.copy()))
+        if len(ring) > k[0] + 1:
+            ring.popleft()
+        x0 = y - k[0]  # output plane whose far suffix starts at y
+        if x0 >= 0 and y < n0:
+            check(x0, ring[0][1], P)
+        if y < n0:
+            P += xh[y]
+    for x0 in range(max(0, n0 - k[0]), n0):  # windows reaching the end: no far suffix
+        # P_{x0} from the end of the ring (the ring holds P_{n0-k0} .. P_{n0})
+        p_x0 = next(p for yy, p in ring if yy == x0)
+        check(x0, p_x0, None)
+    del bc
+    torch.cuda.empty_cache()
+    print(f"C4 box-complement, all {n0} planes: worst err/tol {worst:.3g}")
+
+
+def test_c4_bdbs_whole_array_bit_exact(ex):
+    """C4 BDBS (float32, 1024^3, box 16^3) on bench.py's seeded input against
+    the float32 C oracle (the reference's association) on the whole array: every
+    element bit-identical."""
+    import torch
+
+    x = _bench_input("c4")
+    k = (16, 16, 16)
+    got = ex.bdbs_included(ex.Tensor(ex.Float32AddOps(), x), k).data.cpu().numpy()
+    a = x.cpu().numpy()
+    del x
+    torch.cuda.empty_cache()
+    want = orc.bdbs_included(a, k)
+    assert np.array_equal(got.view(np.uint32), want.view(np.uint32))
+
+
+def test_c4_bdbsc_whole_array(ex):
+    """C4 BDBSC on the whole array: total - BDBS in float64 on the upcast input
+    (the reference algorithm, excluded.py:72-75, 88-90) within the BDBSC
+    contract |got - want| <= D u sum|A|."""
+    import torch
+
+    x = _bench_input("c4")
+    k = (16, 16, 16)
+    got = ex.bdbs_excluded(ex.Tensor(ex.Float32AddOps(), x), k).data.cpu().numpy()
+    a64 = x.cpu().numpy().astype(np.float64)
+    del x
+    torch.cuda.empty_cache()
+    total = float(a64.sum())  # A >= 0: sum|A| = total
+    want = orc.bdbs_included(a64, k)
+    np.subtract(total, want, out=want)
+    D = depth("bdbsc", a64.shape, k)
+    del a64
+    err = float(np.max(np.abs(got.astype(np.float64) - want)))
+    assert err <= D * 2.0**-24 * total, (err, D * 2.0**-24 * total)
