@@ -8,6 +8,9 @@ import torch.distributed as dist
 import paper_2106_00124_b200 as ex
 from paper_2106_00124_b200 import sharded
 
+for k, v in (("RANK", "0"), ("LOCAL_RANK", "0"), ("WORLD_SIZE", "1"), ("MASTER_ADDR", "127.0.0.1"),
+             ("MASTER_PORT", "29533")):
+    os.environ.setdefault(k, v)
 dev = torch.device("cuda", 0)
 torch.cuda.set_device(dev)
 dist.init_process_group("nccl", device_id=dev)
