@@ -32,9 +32,16 @@ def ex():
 def _special_case(rng):
     """Shapes that take the shape-specialised kernels: cubic trailing blocks
     (k_block_cubic: NL 16/28/32/64), two leading axes of 16/28 (k_outer_pair)
-    and rows wider than the fused pair's widest template (row strips)."""
-    kind = int(rng.integers(3))
+    and rows wider than the fused pair's widest template (row strips), the
+    tiled pair (window 32 on the last two axes) and the marginal form of max
+    (any shape; box-complement on max-i64 takes it)."""
+    kind = int(rng.integers(4))
     K = int(rng.choice([2, 4, 8]))
+    if kind == 3:
+        n1, n2 = int(rng.integers(32, 200)), int(rng.integers(32, 300))
+        shape = (int(rng.integers(1, 5)), n1, n2) if rng.random() < 0.5 else (n1, n2)
+        box = (int(rng.choice([1, 3, 32])),) * (len(shape) - 2) + (32, 32)
+        return shape, box
     if kind == 0:
         nl = int(rng.choice([16, 28, 32, 64]))
         m = 3 if nl <= 28 and rng.random() < 0.5 else 2
