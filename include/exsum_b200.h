@@ -212,6 +212,17 @@ int exsum_box_complement_finish(const void *in, void *out, int dtype, int op, in
                                 const int64_t *ext, const int64_t *box, const void *tail,
                                 void *ws, size_t ws_bytes, void *stream);
 
+/* The box-complement tail of a 3-D array per axis-0 shard (R = fold over the
+ * last axis, n0 x n1; T = BC(R, (k0, k1)); a rank holds rows [x0, x0 + n_own)):
+ * stage 0 folds the rank's R rows into R2_own (out, n_own values); stage 1
+ * writes the rank's T rows (out, n_own x n1) from the all-gathered R2 (n0
+ * values) and R's rows [x0, x0 + n_own + min(k0 - 1, n0 - x0 - n_own)) (the
+ * rank's own and the next rank's first k0 - 1, at R); stage -1 checks
+ * eligibility only (EXSUM_ECONFIG: use the all-gathered R and the full route). */
+int exsum_shard_bc_tail(int stage, const void *R, const void *R2, void *out, int dtype, int op,
+                        int64_t n0, int64_t n1, int64_t k0, int64_t k1, int64_t x0, int64_t n_own,
+                        void *stream);
+
 /* Box-complement for max (int64) as per-axis marginals, sharded along axis 0
  * (no halo: the ranks all-reduce sum(ext) values).  ext is the GLOBAL extents;
  * a rank holds global planes [x0, x0 + n_own).

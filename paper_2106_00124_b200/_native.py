@@ -29,6 +29,7 @@ ABI_VERSION = 2
 EXPORTS = (
     "exsum_abi_version",
     "exsum_last_error",
+    "exsum_shard_bc_tail",
     "exsum_shard_idem_workspace_bytes",
     "exsum_shard_idem_marginals",
     "exsum_shard_idem_write",
@@ -132,6 +133,8 @@ def load():
             fn = getattr(L, name)
             fn.argtypes = [vp, vp, ci, ci, ci, i64p, i64p, vp, vp, sz, vp]
             fn.restype = ci
+        L.exsum_shard_bc_tail.argtypes = [ci, vp, vp, vp, ci, ci, i64, i64, i64, i64, i64, i64, vp]
+        L.exsum_shard_bc_tail.restype = ci
         L.exsum_shard_idem_workspace_bytes.argtypes = [ci, ci, ci, i64p, ctypes.POINTER(sz)]
         L.exsum_shard_idem_workspace_bytes.restype = ci
         L.exsum_shard_idem_marginals.argtypes = [vp, vp, ci, ci, ci, i64p, i64, i64, vp, sz, vp]

@@ -1657,6 +1657,45 @@ int exsum_bdbs_finish(const void* in, void* out, int dtype, int op, int d, const
                           stream);
 }
 
+// ---- the box-complement tail of a 3-D array, per axis-0 shard (tail2d.cu) ----
+// stage -1: eligibility only; 0: R2_own[i] = fold of R_own row i (n_own rows);
+// 1: T_own = rows [x0, x0 + n_own) of BC(R, (k0, k1)) from R2 (all n0 rows) and
+// R's rows [x0, x0 + n_own + halo) held at R (halo = min(k0 - 1, n0 - x0 - n_own)).
+int exsum_shard_bc_tail(int stage, const void* R, const void* R2, void* out, int dtype, int op,
+                        int64_t n0, int64_t n1, int64_t k0, int64_t k1, int64_t x0, int64_t n_own,
+                        void* stream) {
+  g_err.clear();
+  int rc = check_types(dtype, op);
+  if (rc) return rc;
+  if (n0 < 1 || n1 < 1 || k0 < 1 || k1 < 1) return fail(EXSUM_EUSAGE, "bad extents or box");
+  if (x0 < 0 || n_own < 0 || x0 + n_own > n0) return fail(EXSUM_EUSAGE, "rows out of range");
+  if (!tail2d_ok(dtype, n0, n1, k0)) return fail(EXSUM_ECONFIG, "no shard tail kernel for this shape");
+  if (stage < 0) return EXSUM_OK;
+  if (n_own == 0) {
+    g_last_launches = 0;
+    return EXSUM_OK;
+  }
+  const int64_t kk0 = k0 < n0 ? k0 : n0, kk1 = k1 < n1 ? k1 : n1;
+  const size_t es = dtype_size(dtype);
+  int n = 0;
+  if (stage == 0) {
+    if (!R || !out) return fail(EXSUM_EUSAGE, "null buffer");
+    n = launch_tail2d_shard(dtype, op, const_cast<void*>(R), out, nullptr, n0, n1, kk0, kk1, 0, n_own,
+                            (cudaStream_t)stream, 0);
+  } else {
+    if (!R || !R2 || !out) return fail(EXSUM_EUSAGE, "null buffer");
+    // R and out addressed by the global row: shift the bases back by x0 rows
+    const char* rv = static_cast<const char*>(R) - (size_t)(x0 * n1) * es;
+    char* ov = static_cast<char*>(out) - (size_t)(x0 * n1) * es;
+    n = launch_tail2d_shard(dtype, op, rv, const_cast<void*>(R2), ov, n0, n1, kk0, kk1, x0,
+                            x0 + n_own, (cudaStream_t)stream, 1);
+  }
+  if (n < 0) return fail(EXSUM_ECONFIG, "no shard tail kernel for this dtype/operator");
+  g_last_launches = n;
+  g_total_launches += n;
+  return cuda_check("shard tail");
+}
+
 // ---- box-complement for max as marginals, sharded along axis 0 (idem_max.cu) ----
 static int idem_shard_check(int dtype, int op, int d, const int64_t* ext, int64_t x0,
                             int64_t n_own) {

@@ -65,6 +65,13 @@ int launch_complement(int dtype, const void* in, void* out, int64_t N, const voi
 int tail2d_ok(int dtype, int64_t n0, int64_t n1, int64_t k0);
 int launch_tail2d(int dtype, int op, const void* part, int64_t ppr, void* R, void* R2, void* Tout,
                   int64_t n0, int64_t n1, int64_t k0, int64_t k1, cudaStream_t s, int stage);
+// The tail of one axis-0 shard (sharded box-complement): stage 0 R2[i] = fold
+// of R row i for the rows [gb, ge) held at R (local indexing); stage 1 the rows
+// [gb, ge) of T = BC(R) from R2 (all n0 rows) and R's rows [gb, ge + k0 - 1)
+// (the shard's own and its halo), R and Tout addressed by the global row.
+int launch_tail2d_shard(int dtype, int op, const void* R, void* R2, void* Tout, int64_t n0,
+                        int64_t n1, int64_t k0, int64_t k1, int64_t gb, int64_t ge, cudaStream_t s,
+                        int stage);
 
 // R[r] = (+)_x in[r, x] for rows of length n (box-complement reduction of the
 // peeled last axis).

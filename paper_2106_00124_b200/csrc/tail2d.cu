@@ -143,7 +143,9 @@ __device__ __forceinline__ T group_fold(T v, T* sh) {
 template <class T, class Op, int C>
 __global__ void __launch_bounds__(kGroupThreads)
 k_tail_group(const T* __restrict__ R, const T* __restrict__ R2, T* __restrict__ Tout, int n0,
-             int n1, int k0, int k1) {
+             int n1, int k0, int k1, int gb, int ge) {
+  // rows [gb, ge) of T (a shard: its own rows; R and Tout are indexed by the
+  // global row, only rows >= gb are touched)
   constexpr int P = pitch<C>();
   constexpr int G = kGroup;
   __shared__ __align__(16) T Wt[G][P];
@@ -153,10 +155,10 @@ k_tail_group(const T* __restrict__ R, const T* __restrict__ R2, T* __restrict__ 
   const T ident = Op::template identity<T>();
   const int lane = threadIdx.x & 31;
   const int warp = threadIdx.x >> 5;
-  const int ngroups = (n0 + G - 1) / G;
+  const int ngroups = (ge - gb + G - 1) / G;
   for (int grp = blockIdx.x; grp < ngroups; grp += gridDim.x) {
-    const int g0 = grp * G;
-    const int gm = n0 - g0 < G ? n0 - g0 : G;          // rows in this group
+    const int g0 = gb + grp * G;
+    const int gm = ge - g0 < G ? ge - g0 : G;          // rows in this group
     const int gk = G <= k0 ? G : 1;                     // middle form needs G <= k0
     // ---- T1: P2[x0-1] (+) S2[x0+k0] for the group's rows ----
     T pre = ident;
@@ -301,6 +303,10 @@ int tail_chunk(int64_t n1) {
 }
 
 template <class T, class Op, int C>
+int go_group_c(const void* R, const void* R2, void* Tout, int64_t n0, int64_t n1, int64_t k0,
+               int64_t k1, int64_t gb, int64_t ge, cudaStream_t s);
+
+template <class T, class Op, int C>
 int go_tail_c(const void* part, int64_t ppr, void* R, void* R2, void* Tout, int64_t n0, int64_t n1,
               int64_t k0, int64_t k1, cudaStream_t s, int stage) {
   if (stage == 0) {
@@ -310,11 +316,19 @@ int go_tail_c(const void* part, int64_t ppr, void* R, void* R2, void* Tout, int6
     k_tail_rows<T, Op><<<(unsigned)g1, kTailThreads, 0, s>>>((const T*)part, ppr, (T*)R, (T*)R2, n0, n1);
     return 1;
   }
-  int64_t g2 = (n0 + kGroup - 1) / kGroup;
+  return go_group_c<T, Op, C>(R, R2, Tout, n0, n1, k0, k1, 0, n0, s);
+}
+
+template <class T, class Op, int C>
+int go_group_c(const void* R, const void* R2, void* Tout, int64_t n0, int64_t n1, int64_t k0,
+               int64_t k1, int64_t gb, int64_t ge, cudaStream_t s) {
+  int64_t g2 = (ge - gb + kGroup - 1) / kGroup;
   const int64_t cap2 = (int64_t)num_sms() * 16;
   if (g2 > cap2) g2 = cap2;
+  if (g2 < 1) return 0;
   k_tail_group<T, Op, C><<<(unsigned)g2, kGroupThreads, 0, s>>>((const T*)R, (const T*)R2, (T*)Tout,
-                                                                (int)n0, (int)n1, (int)k0, (int)k1);
+                                                                (int)n0, (int)n1, (int)k0, (int)k1,
+                                                                (int)gb, (int)ge);
   return 1;
 }
 
@@ -334,7 +348,44 @@ int go_tail(const void* part, int64_t ppr, void* R, void* R2, void* Tout, int64_
   return -1;
 }
 
+// A shard of the tail: stage 0 R2[i] = fold of R row i (n_rows rows of R);
+// stage 1 T rows [gb, ge) with R and Tout indexed by the global row.
+template <class T, class Op>
+int go_tail_shard(const void* R, void* R2, void* Tout, int64_t n0, int64_t n1, int64_t k0,
+                  int64_t k1, int64_t gb, int64_t ge, cudaStream_t s, int stage) {
+  if (stage == 0) {
+    const int64_t rows = ge - gb;
+    if (rows <= 0) return 0;
+    int64_t g1 = rows;
+    const int64_t cap = (int64_t)num_sms() * 8;
+    if (g1 > cap) g1 = cap;
+    k_tail_rows<T, Op><<<(unsigned)g1, kTailThreads, 0, s>>>(nullptr, 0, (T*)R, (T*)R2, rows, n1);
+    return 1;
+  }
+  switch (tail_chunk(n1)) {
+    case 1: return go_group_c<T, Op, 1>(R, R2, Tout, n0, n1, k0, k1, gb, ge, s);
+    case 2: return go_group_c<T, Op, 2>(R, R2, Tout, n0, n1, k0, k1, gb, ge, s);
+    case 4: return go_group_c<T, Op, 4>(R, R2, Tout, n0, n1, k0, k1, gb, ge, s);
+    case 8: return go_group_c<T, Op, 8>(R, R2, Tout, n0, n1, k0, k1, gb, ge, s);
+    case 16: return go_group_c<T, Op, 16>(R, R2, Tout, n0, n1, k0, k1, gb, ge, s);
+    case 32:
+      if constexpr (sizeof(T) == 4) return go_group_c<T, Op, 32>(R, R2, Tout, n0, n1, k0, k1, gb, ge, s);
+      return -1;
+  }
+  return -1;
+}
+
 }  // namespace
+
+int launch_tail2d_shard(int dtype, int op, const void* R, void* R2, void* Tout, int64_t n0,
+                        int64_t n1, int64_t k0, int64_t k1, int64_t gb, int64_t ge, cudaStream_t s,
+                        int stage) {
+  if (dtype == F32 && op == ADD) return go_tail_shard<float, OpAdd>(R, R2, Tout, n0, n1, k0, k1, gb, ge, s, stage);
+  if (dtype == F64 && op == ADD) return go_tail_shard<double, OpAdd>(R, R2, Tout, n0, n1, k0, k1, gb, ge, s, stage);
+  if (dtype == I64 && op == ADD) return go_tail_shard<i64, OpAdd>(R, R2, Tout, n0, n1, k0, k1, gb, ge, s, stage);
+  if (dtype == I64 && op == MAX) return go_tail_shard<i64, OpMax>(R, R2, Tout, n0, n1, k0, k1, gb, ge, s, stage);
+  return -2;
+}
 
 int tail2d_ok(int dtype, int64_t n0, int64_t n1, int64_t k0) {
   const char* e = getenv("EXSUM_TAIL2D");  // 0: the recursive tail (measurement)

@@ -13,8 +13,11 @@ cross-rank data are:
 * BDBSC: the scalar total -- per-rank partials are all-gathered and combined
   in rank order (deterministic; float data folds in float64);
 * box-complement: R = fold over the last axis (one value per row, N/n_{d-1}
-  elements) is all-gathered; every rank computes the tail BC(R, k[:-1]) of the
-  small array redundantly and keeps its own rows.
+  elements).  For d = 3 every rank computes only its own rows of the tail
+  T = BC(R, k[:-1]): it needs R2 (the fold of R's rows: n0 values, all-gathered)
+  and the next rank's first k0-1 rows of R (a halo exchange like the array's);
+  otherwise R is all-gathered and every rank computes the whole tail
+  redundantly, keeping its own rows.
 
 Everything else (the remaining windowed passes, the row round) is local.
 
@@ -162,6 +165,36 @@ class CudaEngine:
             _native.i64_array(box), tail.contiguous().data_ptr(), ws.data_ptr(), ws.numel(),
             self._stream()))
         return out
+
+    def bc_tail_ok(self, ext, k):
+        """Whether the per-shard tail applies (3-D: R is n0 x n1)."""
+        if len(ext) != 3:
+            return False
+        rc = self.L.exsum_shard_bc_tail(-1, None, None, None, _native.DTYPE[self.dtype_name],
+                                         _native.OP[self.op], int(ext[0]), int(ext[1]), int(k[0]),
+                                         int(k[1]), 0, 0, None)
+        return rc == 0
+
+    def bc_tail_r2(self, R_own, ext, k):
+        """The fold of each of this rank's R rows (n_own values)."""
+        torch = self.torch
+        n_own = int(R_own.shape[0])
+        r2 = torch.empty(n_own, dtype=R_own.dtype, device=self.device)
+        _native.check(self.L.exsum_shard_bc_tail(
+            0, R_own.contiguous().data_ptr() if n_own else None, None,
+            r2.data_ptr() if n_own else None, _native.DTYPE[self.dtype_name], _native.OP[self.op],
+            int(ext[0]), int(ext[1]), int(k[0]), int(k[1]), 0, n_own, self._stream()))
+        return r2
+
+    def bc_tail_rows(self, R_ext, R2, ext, k, x0, n_own):
+        """This rank's rows of the tail T = BC(R) from R's rows [x0, x0+n_own+halo)."""
+        torch = self.torch
+        T = torch.empty((n_own, int(ext[1])), dtype=R_ext.dtype, device=self.device)
+        _native.check(self.L.exsum_shard_bc_tail(
+            1, R_ext.contiguous().data_ptr() if n_own else None, R2.contiguous().data_ptr(),
+            T.data_ptr() if n_own else None, _native.DTYPE[self.dtype_name], _native.OP[self.op],
+            int(ext[0]), int(ext[1]), int(k[0]), int(k[1]), int(x0), int(n_own), self._stream()))
+        return T
 
     def idem_ok(self, ext):
         """Whether the per-axis marginal form applies (max over int64, d >= 2,
@@ -349,6 +382,10 @@ class ShardedRunner:
         # max over int64: the per-axis marginal form -- no halo, no tail
         self.idem = (route == "box-complement" and op == "max" and hasattr(self.engine, "idem_ok")
                      and self.engine.idem_ok(self.ext))
+        # 3-D box-complement: each rank computes only its own rows of the tail
+        self.own_tail = (route == "box-complement" and not self.idem
+                         and hasattr(self.engine, "bc_tail_ok")
+                         and self.engine.bc_tail_ok(self.ext[:-1], self.k[:-1]))
 
     def local_shape(self):
         return (self.n_own + self.halo,) + self.ext[1:]
@@ -426,9 +463,31 @@ class ShardedRunner:
             return torch.stack(self.comm.all_gather_scalars(extra)).sum(dim=0)
         if self.route == "box-complement":
             counts = [self.plan.bounds(q)[1] - self.plan.bounds(q)[0] for q in range(self.world)]
+            if self.own_tail:
+                return self.own_tail_rows(extra, counts)
             R = self.comm.all_gather_rows(extra, counts)
             return self.engine.box_complement(R, self.k[:-1])  # tail T, computed redundantly
         return None
+
+    def own_tail_rows(self, R_own, counts, R_halo=None):
+        """This rank's rows of T: R2 all-gathered (n0 values), the next rank's
+        first k0-1 rows of R by the halo exchange (R_halo given: loopback)."""
+        import torch
+
+        ext2, k2 = self.ext[:-1], self.k[:-1]
+        r2 = self.engine.bc_tail_r2(R_own, ext2, k2)
+        R2 = self.comm.all_gather_rows(r2, counts)
+        R_ext = torch.empty((self.n_own + self.halo,) + tuple(R_own.shape[1:]), dtype=R_own.dtype,
+                            device=R_own.device)
+        if self.n_own:
+            R_ext[:self.n_own] = R_own
+        if R_halo is not None:
+            if self.halo:
+                R_ext[self.n_own:] = R_halo
+        else:
+            for req in self.comm.start_halo(self.plan, R_ext, self.n_own):
+                req.wait()
+        return self.engine.bc_tail_rows(R_ext, R2, ext2, k2, self.start, self.n_own)
 
     def stage2(self, y, combined):
         if y is None:
@@ -437,7 +496,8 @@ class ShardedRunner:
             return self.engine.bdbs_finish(y, self.k, None)
         if self.route == "bdbsc":
             return self.engine.bdbs_finish(y, self.k, combined.reshape(1).contiguous())
-        return self.engine.bc_finish(y, self.k, combined[self.start:self.end])
+        tail = combined if self.own_tail else combined[self.start:self.end]
+        return self.engine.bc_finish(y, self.k, tail)
 
 
 def _torch_dtype(engine):
@@ -500,6 +560,16 @@ def run_loopback(route, ops, a, box, world, engine, split=True):
         extras.append(r.local_extra(e, a.device))
     comm.extras = extras
     outs = []
+    if runners and runners[0].own_tail:
+        counts = [r.n_own for r in runners]
+        R_all = torch.cat([e[:c] for e, c in zip(extras, counts)], dim=0)
+        comm.extras = [r.engine.bc_tail_r2(e, r.ext[:-1], r.k[:-1]) for r, e in zip(runners, extras)]
+        for r, y in zip(runners, ys):
+            T = r.own_tail_rows(extras[runners.index(r)], counts, R_halo=R_all[r.end:r.end + r.halo])
+            o = r.stage2(y, T)
+            if o is not None:
+                outs.append(o)
+        return torch.cat(outs, dim=0)
     combined = runners[0].combine(extras[0], a.device) if world > 0 else None
     for r, y in zip(runners, ys):
         o = r.stage2(y, combined)

@@ -73,6 +73,41 @@ class OracleEngine:
             out = comb(out, tail.numpy()[..., None])
         return torch.from_numpy(np.ascontiguousarray(out))
 
+    # the per-shard tail of a 3-D box-complement (sharded.CudaEngine.bc_tail_*)
+    def bc_tail_ok(self, ext, k):
+        return len(ext) == 2
+
+    def bc_tail_r2(self, R_own, ext, k):
+        a = R_own.contiguous().numpy()
+        red = a.max(axis=-1) if self.op == "max" else a.sum(axis=-1, dtype=a.dtype)
+        return torch.from_numpy(np.ascontiguousarray(red))
+
+    def bc_tail_rows(self, R_ext, R2, ext, k, x0, n_own):
+        """T rows [x0, x0+n_own) of BC(R): T1 from R2 (1-D excluded window),
+        the window of R along axis 0, its row round along axis 1."""
+        n0, n1 = ext
+        k0, k1 = min(k[0], n0), min(k[1], n1)
+        Rx = R_ext.contiguous().numpy()
+        r2 = R2.contiguous().numpy()
+        comb = np.maximum if self.op == "max" else np.add
+        ident = np.iinfo(np.int64).min if self.op == "max" else Rx.dtype.type(0)
+        out = np.empty((n_own, n1), dtype=Rx.dtype)
+        with np.errstate(over="ignore"):
+            for i in range(n_own):
+                x = x0 + i
+                t1 = ident
+                for y in list(range(0, x)) + list(range(min(x + k0, n0), n0)):
+                    t1 = comb(t1, r2[y])
+                w = Rx[i]
+                for y in range(x + 1, min(x + k0, n0)):
+                    w = comb(w, Rx[y - x0])
+                for c in range(n1):
+                    v = t1
+                    for cc in list(range(0, c)) + list(range(min(c + k1, n1), n1)):
+                        v = comb(v, w[cc])
+                    out[i, c] = v
+        return torch.from_numpy(out)
+
     # the per-axis marginal form for max (sharded.CudaEngine.idem_*): the
     # rank's marginals of its planes, then its output planes from the global ones
     def idem_ok(self, ext):
