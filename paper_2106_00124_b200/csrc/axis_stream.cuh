@@ -39,6 +39,21 @@ namespace exsum {
 #ifndef AS_DEFER
 #define AS_DEFER 0  // 1: unit u's output rows leave during unit u+1 through a per-thread stage
 #endif
+#ifndef AS_GRID_MULT
+#define AS_GRID_MULT 4  // grid cap in resident CTAs (items are grid-strided)
+#endif
+#ifndef AS_PSTRIDE
+#define AS_PSTRIDE 1  // measurement only: strip order multiplier (must be coprime to the strip count)
+#endif
+#ifndef AS_NSEG_MIN
+#define AS_NSEG_MIN 1  // measurement only: at least this many axis segments
+#endif
+#ifndef AS_SEG_FAST
+#define AS_SEG_FAST 0  // measurement only: 1 makes the segment the fastest item index
+#endif
+#ifndef AS_NO_C32
+#define AS_NO_C32 0  // measurement only: 1 keeps 4-byte types on the 512-column strip
+#endif
 
 template <class T, class Op, int C, int K1, int EX>
 __global__ void __launch_bounds__(32 * C / (16 / sizeof(T)), 1)
@@ -68,14 +83,14 @@ k_axis_stream(const T* __restrict__ in, T* __restrict__ out, int64_t outer, int6
   const int64_t last_bs = (int64_t)K1 * ((n1 - 1) / K1);
   const int64_t strips = inner / N2;
   const int64_t items = outer * strips * nseg;
-  const int64_t rows_total = outer * nout * (inner / row_len);  // rows of the last axis
   Acc tacc[VE];
 #pragma unroll
   for (int j = 0; j < VE; ++j) tacc[j] = Op::template identity<Acc>();
 
   for (int64_t item = blockIdx.x; item < items; item += gridDim.x) {
-    const int64_t strip = item % strips;
-    const int64_t rest = item / strips;
+    const int64_t it2 = AS_SEG_FAST ? (item % nseg) * (outer * strips) + item / nseg : item;
+    const int64_t strip = AS_PSTRIDE == 1 ? it2 % strips : (it2 % strips) * AS_PSTRIDE % strips;
+    const int64_t rest = it2 / strips;
     const int64_t o = rest % outer;
     const int64_t seg = rest / outer;
     const int64_t xs = seg * seg_len;  // multiple of U
@@ -157,8 +172,8 @@ k_axis_stream(const T* __restrict__ in, T* __restrict__ out, int64_t outer, int6
       if (r < len) cur[r] = *reinterpret_cast<const VT*>(raw + col + r * N2);
     issue(u0 + AS_RING);
 
-    int prev_w = 0;        // AS_DEFER: stage rows [0, prev_w) still hold unit prev_us's output
-    int64_t prev_us = 0;
+    [[maybe_unused]] int prev_w = 0;  // AS_DEFER: stage rows [0, prev_w) still hold unit prev_us's output
+    [[maybe_unused]] int64_t prev_us = 0;
     auto flush = [&](int from, int to) {
       for (int r = from; r < to; ++r)
         st_stream<T, VE>(dst + (prev_us + r) * inner, *reinterpret_cast<const VT*>(stg + r * N2 + col));
@@ -305,11 +320,12 @@ int go_axis_stream_c(const T* in, T* out, int64_t outer, int64_t n, int64_t inne
   const int64_t lines = outer * strips;
   const int64_t nunits = (nout + U - 1) / U;
   int64_t nseg = pick_segments(lines, nunits, per_sm);
+  if (nseg < AS_NSEG_MIN && nunits >= AS_NSEG_MIN) nseg = AS_NSEG_MIN;
   const int64_t seg_len = U * ((nunits + nseg - 1) / nseg);
   nseg = (nout + seg_len - 1) / seg_len;
   const int64_t items = lines * nseg;
   int64_t grid = items;
-  const int64_t cap = (int64_t)num_sms() * per_sm * 4;
+  const int64_t cap = (int64_t)num_sms() * per_sm * AS_GRID_MULT;
   if (EX == 2 && cap > ex->cap) return -1;
   if (grid > cap) grid = cap;
   ensure_smem((const void*)k_axis_stream<T, Op, C, K1, EX>, smem);
@@ -368,7 +384,7 @@ int go_axis_stream(const T* in, T* out, int64_t outer, int64_t n, int64_t inner,
   const int64_t nout = (ex && ex->n_out >= 0) ? ex->n_out : n;
   if (nout != n && outer != 1) return -1;
   if constexpr (sizeof(T) == 4) {
-    if (inner % 1024 == 0 && (!ex || ex->kind != 1 || ex->row_len % 1024 == 0))
+    if (!AS_NO_C32 && inner % 1024 == 0 && (!ex || ex->kind != 1 || ex->row_len % 1024 == 0))
       return pick_axis_ex<T, Op, 32>(in, out, outer, n, inner, nout, k, total, s, ex);
   }
   if (inner % 512 == 0 && (!ex || ex->kind != 1 || ex->row_len % 512 == 0))

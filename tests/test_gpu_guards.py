@@ -24,7 +24,17 @@ SHAPES = [
     ((64, 3), (17, 2)), ((2, 3, 4), (2, 2, 2)), ((13, 7, 9), (3, 1, 4)), ((5, 8, 256), (4, 4, 4)),
     ((3, 16, 1024), (16, 16, 16)), ((130, 4, 33), (128, 4, 1)), ((6, 6, 6, 6), (2, 3, 1, 6)),
     ((2, 3, 2, 3, 2), (2, 2, 2, 2, 2)), ((300, 2), (37, 1)), ((2, 5000), (1, 600)),
+    # round-2 kernels: the tiled pair (window 32, element-granular staging), the TMA
+    # tensor pass (k = 128 along a strided axis), the 3-D box-complement tail, row
+    # strips wider than the fused pair's templates, trailing cubic blocks, the
+    # leading-axis pair
+    ((45, 33), (32, 32)), ((3, 70, 200), (1, 32, 32)), ((256, 2, 64), (128, 2, 1)),
+    ((40, 24, 256), (8, 8, 8)), ((3, 3000), (2, 16)), ((70, 16, 16), (4, 4, 4)),
+    ((28, 28, 32), (4, 4, 1)),
 ]
+# profiler scopes the aligned sweep must reach (every kernel family of the routes)
+REQUIRED = {"pass_strided", "pass_rows", "fused_pair", "tile_pair", "idem_scan", "idem_bcast",
+            "tail_rows", "tail_group", "block_fused", "outer_pair", "total"}
 
 
 @pytest.fixture(scope="module")
@@ -60,6 +70,8 @@ def test_no_writes_outside_the_call_regions(ex, shift):
     L = _native.load()
     rng = np.random.default_rng(31)
     count = 0
+    _native.profile_enable(True)
+    seen = set()
     for shape, box, mono, route in _cases():
         dt = np.dtype(np.float32 if mono == "add-f32" else np.float64 if mono == "add-f64"
                       else np.int64)
@@ -94,6 +106,8 @@ def test_no_writes_outside_the_call_regions(ex, shift):
                           dws.data_ptr() + GUARD * 8, wsn, torch.cuda.current_stream().cuda_stream)
         _native.check(rc)
         torch.cuda.synchronize()
+        seen.update(n for n, _, _ in _native.profile_records())
+        _native.profile_enable(True)  # clears the records
         h_out = dout.cpu().numpy()
         assert np.array_equal(din.cpu().numpy().view(np.uint8), host_in.view(np.uint8)), \
             ("input modified", shape, box, mono, route)
@@ -116,7 +130,11 @@ def test_no_writes_outside_the_call_regions(ex, shift):
         else:
             assert np.array_equal(got, want), (shape, box, mono, route)
         count += 1
+    _native.profile_enable(False)
     assert count > 300
+    if not shift:
+        print("scopes:", sorted(seen))
+        assert REQUIRED <= seen, sorted(REQUIRED - seen)
 
 
 def test_building_block_guards(ex):
