@@ -48,6 +48,13 @@ namespace exsum {
 #ifndef FP_NARROW_C
 #define FP_NARROW_C 8
 #endif
+// largest window along the row that takes 256-column strips on long rows
+#ifndef FP_STRIP_NARROW_K8
+#define FP_STRIP_NARROW_K8 8
+#endif
+#ifndef FP_STRIP_NARROW_K4
+#define FP_STRIP_NARROW_K4 2
+#endif
 // the stores of unit u's rows run inside unit u+1's axis-(d-2) pass, each row
 // right before its stage slot is rewritten (interleaving the streaming stores
 // with the compute instead of a store-only loop after the row op).  Measured
@@ -78,10 +85,13 @@ template <int CV>
 __device__ __forceinline__ int fp_swz(int v) {
   return v ^ ((v >> 3) & (CV - 1));
 }
-__host__ __device__ constexpr bool fp_swizzled(int CV, int MODE) { return CV < 8 && MODE != ROW_EXCL; }
+// (strips keep the padded layout: their halo lives in a 33rd chunk)
+__host__ __device__ constexpr bool fp_swizzled(int CV, int MODE, bool STRIP = false) {
+  return CV < 8 && MODE != ROW_EXCL && !STRIP;
+}
 // chunk stride in 16-byte vectors: CV when swizzled, else padded to odd
-__host__ __device__ constexpr int fp_chunk_stride(int CV, int MODE) {
-  return fp_swizzled(CV, MODE) ? CV : ((CV + 1) | 1);
+__host__ __device__ constexpr int fp_chunk_stride(int CV, int MODE, bool STRIP = false) {
+  return fp_swizzled(CV, MODE, STRIP) ? CV : ((CV + 1) | 1);
 }
 
 template <class T, class Op, int C, int K1, int MODE, int TV, bool STRIP>
@@ -109,8 +119,8 @@ k_fused_pair(const T* __restrict__ in, T* __restrict__ out, int64_t outer, int64
   // side) except under the prefix/suffix row op, whose many chunk accesses
   // would each pay the lane-dependent swizzle in address arithmetic (C2 max
   // 0.084 -> 0.090 ms); padded chunks (odd stride) otherwise
-  constexpr bool SWZ = fp_swizzled(CV, MODE);
-  constexpr int CH = fp_chunk_stride(CV, MODE) * VE;  // chunk stride (elements)
+  constexpr bool SWZ = fp_swizzled(CV, MODE, STRIP);
+  constexpr int CH = fp_chunk_stride(CV, MODE, STRIP) * VE;  // chunk stride (elements)
   constexpr int HV = STRIP ? (K1 - 1 + VE - 1) / VE : 0;  // halo vectors per row
   constexpr int RAWP = N2 + HV * VE;                 // ring row pitch
   constexpr int ROWP = (STRIP ? 33 : 32) * CH;       // stage row length (elements; chunk 32 = halo)
@@ -628,7 +638,7 @@ int go_pair(const T* in, T* out, int64_t outer, int64_t n1, int64_t kx,
   constexpr int NT = N2 / TV;
   constexpr int CV = C / VE;
   constexpr int HV = STRIP ? (K1 - 1 + VE - 1) / VE : 0;
-  constexpr int ROWP = (STRIP ? 33 : 32) * fp_chunk_stride(CV, MODE) * VE;
+  constexpr int ROWP = (STRIP ? 33 : 32) * fp_chunk_stride(CV, MODE, STRIP) * VE;
   constexpr int U = fp_unit_rows(C, K1);
   constexpr int NTA = NT + (STRIP ? 32 : 0);
   const int64_t nstrips = STRIP ? n2full / N2 : 1;
@@ -675,6 +685,14 @@ int go_fused(const T* in, T* out, int64_t outer, int64_t n1, int64_t n2, int64_t
   if (mode == ROW_WIN) {
     // rows longer than the widest row template: strips of it with a halo
     constexpr int CW = sizeof(T) == 4 ? 32 : 16;
+    // small windows on rows longer than the widest template: 256-column strips
+    // (4-8-row units, a 25-50 KB ring and stage: 4 CTAs per SM instead of one
+    // 200 KB CTA of 9 warps).  Measured (tools/variant_time.py): 8-byte 4096^2
+    // box 4^2 max 75.8 -> 61.4 us, + 71.7 -> 57.3 us, box 8^2 max 90.6 -> 74.2
+    // us; float32 only for k = 2 (64x2048x2048 box 2^3 pair 0.404 -> 0.361 ms;
+    // 4096^2 box 4^2 34.8 -> 36.9 us and box 8^2 35 -> 59 us stay on 1024-wide strips)
+    if (n2 > 32 * CW && n2 % 256 == 0 && k1 <= (sizeof(T) == 8 ? FP_STRIP_NARROW_K8 : FP_STRIP_NARROW_K4))
+      return pick_k1<T, Op, 8, ROW_WIN, true>(in, out, outer, n1, k1, 0, total, nullptr, s, n2);
     if (n2 > 32 * CW && n2 % (32 * CW) == 0)
       return pick_k1<T, Op, CW, ROW_WIN, true>(in, out, outer, n1, k1, 0, total, nullptr, s, n2);
     switch (n2) {

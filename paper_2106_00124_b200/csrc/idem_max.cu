@@ -24,13 +24,15 @@
 //                 with equal leading coordinates (segmented warp fold) and
 //                 atomically max'ed into M_a (a < d-1); per column the fold over
 //                 the CTA's rows, atomically into M_{d-1};
-//   k_idem_bcast  one write of out: every CTA first builds F (a warp per axis:
-//                 chunk folds, warp scans for the carries, suffix stage, then
-//                 P[i-1] (+) S[i+k]) from the marginals in shared memory, then
-//                 per row the fold of the leading F_a and out = that (+)
-//                 F_{d-1}[column] -- 16-byte streaming stores.
+//   k_idem_bcast  one write of out: a grid of 2 CTAs per SM; every CTA first
+//                 builds F (a warp per axis: chunk folds, warp scans for the
+//                 carries, suffix stage, then P[i-1] (+) S[i+k]) from the
+//                 marginals in shared memory, then its warps take units of 4
+//                 rows in turn: per row the fold of the leading F_a and
+//                 out = that (+) F_{d-1}[column] -- 16-byte streaming stores.
 // DRAM traffic 2 N s against 4 N s for the slab route (C2 box-complement max
-// 0.127 -> 0.059 ms); a read-all-then-write-all schedule is the floor for any
+// 0.127 -> 0.055 ms; a plain read of the same 134 MB takes 29-31 us and a plain
+// write 25-27 us on B200, tools/bw_probe.cu); a read-all-then-write-all schedule is the floor for any
 // excluded sum (every output depends on the whole input).
 #include <stdlib.h>
 
@@ -43,7 +45,10 @@ namespace exsum {
 
 namespace {
 
-constexpr int kIdemThreads = 256;
+#ifndef IDEM_THREADS
+#define IDEM_THREADS 256
+#endif
+constexpr int kIdemThreads = IDEM_THREADS;
 constexpr int kIdemWarps = kIdemThreads / 32;
 #ifndef IDEM_RBU
 #define IDEM_RBU 16
@@ -167,7 +172,7 @@ __device__ __forceinline__ void idem_rows(const T* __restrict__ src, int64_t nl,
 // per column the fold over the CTA's rows into the last-axis marginal (atomic
 // max on the biased image).
 template <class T, class Op, int VE, int NV>
-__global__ void __launch_bounds__(kIdemThreads, NV >= 8 ? 2 : IDEM_MINB)
+__global__ void __launch_bounds__(kIdemThreads, (NV >= 8 ? 2 : IDEM_MINB) * 256 / kIdemThreads)
 k_idem_scan(const T* __restrict__ in, unsigned long long* __restrict__ Mu, IdemShape s,
             int64_t nstrip, int64_t nrb) {
   typedef Vec<T, VE> VT;
@@ -226,6 +231,21 @@ k_idem_scan(const T* __restrict__ in, unsigned long long* __restrict__ Mu, IdemS
   }
 }
 
+template <class T, class Op, int VE, int NV, int RB>
+__device__ __forceinline__ void idem_bcast_unit(const T* F, T* __restrict__ out, const IdemShape& s,
+                                                int64_t strip, int64_t rb, int lane);
+
+// The broadcast's grid: IDEM_BGRID CTAs per SM (0: one CTA per 8 row
+// blocks of the scan's tiling) over warp units of IDEM_BRB rows.  C2 (256^3):
+// 2 / 4 -> broadcast 33.1 -> 29.1 us (0/16 leaves the SMs 3-4 CTAs each, and
+// every CTA builds the tables; 1-2 per SM with 4-row units balance to ~1%).
+#ifndef IDEM_BGRID
+#define IDEM_BGRID 2
+#endif
+#ifndef IDEM_BRB
+#define IDEM_BRB 4
+#endif
+
 // One write of out.  Prologue (every CTA, redundantly -- the tables are at
 // most kIdemMaxSum elements): the marginals from Mu into shared memory, then a
 // warp per axis builds F_a in place: lane chunks, warp scans of the chunk
@@ -237,8 +257,6 @@ template <class T, class Op, int VE, int NV>
 __global__ void __launch_bounds__(kIdemThreads)
 k_idem_bcast(const unsigned long long* __restrict__ Mu, T* __restrict__ out, IdemShape s,
              int64_t nstrip, int64_t nrb, unsigned long long flip) {
-  typedef Vec<T, VE> VT;
-  constexpr int W = 32 * VE * NV;
   extern __shared__ __align__(16) unsigned char smem[];
   T* F = reinterpret_cast<T*>(smem);  // [S]: M, then F
   T* Ss = F + s.S;                    // [S]: inclusive suffixes
@@ -280,12 +298,31 @@ k_idem_bcast(const unsigned long long* __restrict__ Mu, T* __restrict__ out, Ide
     }
   }
   __syncthreads();
+#if IDEM_BGRID
+  // a grid of IDEM_BGRID CTAs per SM: warp units (row block, strip) taken in
+  // turn, the tables built once per CTA
+  const int64_t nrb_b = (s.rows + IDEM_BRB - 1) / IDEM_BRB;
+  for (int64_t u = (int64_t)blockIdx.x * kIdemWarps + warp; u < nrb_b * nstrip;
+       u += (int64_t)gridDim.x * kIdemWarps) {
+    idem_bcast_unit<T, Op, VE, NV, IDEM_BRB>(F, out, s, u % nstrip, u / nstrip, lane);
+  }
+#else
   const int64_t strip = blockIdx.x % nstrip;
   const int64_t rb = (blockIdx.x / nstrip) * kIdemWarps + warp;
   if (rb >= nrb) return;
+  idem_bcast_unit<T, Op, VE, NV, kRbu>(F, out, s, strip, rb, lane);
+#endif
+}
+
+template <class T, class Op, int VE, int NV, int RB>
+__device__ __forceinline__ void idem_bcast_unit(const T* F, T* __restrict__ out, const IdemShape& s,
+                                                int64_t strip, int64_t rb, int lane) {
+  typedef Vec<T, VE> VT;
+  constexpr int W = 32 * VE * NV;
+  const T ident = Op::template identity<T>();
   const int64_t c0 = strip * W;
-  const int64_t r0 = rb * kRbu;
-  const int nr = (int)min((int64_t)kRbu, s.rows - r0);
+  const int64_t r0 = rb * RB;
+  const int nr = (int)min((int64_t)RB, s.rows - r0);
   T crow = ident;
   if (lane < nr) {
     int64_t r = s.row_off + r0 + lane;
@@ -328,7 +365,11 @@ void launch_stage(const T* in, T* out, const IdemShape& s, const IdemTiling& t,
   } else {
     const size_t sm = (size_t)2 * s.S * sizeof(T);
     ensure_smem((const void*)k_idem_bcast<T, Op, VE, NV>, sm);
-    k_idem_bcast<T, Op, VE, NV><<<grid, kIdemThreads, sm, st>>>(Mu, out, s, t.nstrip, t.nrb, flip);
+    unsigned bgrid = grid;
+#if IDEM_BGRID
+    bgrid = (unsigned)std::min<int64_t>(grid, (int64_t)num_sms() * IDEM_BGRID);
+#endif
+    k_idem_bcast<T, Op, VE, NV><<<bgrid, kIdemThreads, sm, st>>>(Mu, out, s, t.nstrip, t.nrb, flip);
   }
 }
 

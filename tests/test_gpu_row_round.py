@@ -108,6 +108,13 @@ STRIP_CASES = [
     ((19, 1536), (16, 16), "add-f64"),
     ((19, 1536), (2, 2), "max-i64"),
     ((2, 40, 4096), (2, 8, 8), "add-f64"),
+    # 256-column strips (8-byte k <= 8, float32 k = 2 on rows past the widest template)
+    ((23, 1536), (4, 4), "max-i64"),
+    ((9, 1280), (8, 8), "add-i64"),
+    ((17, 4096), (8, 8), "add-f64"),
+    ((5, 7, 2048), (1, 2, 2), "add-f32"),
+    ((3, 33, 1280), (2, 2, 2), "add-f32"),
+    ((41, 768), (2, 2), "max-i64"),
 ]
 
 

@@ -1,6 +1,7 @@
 """Run one route a few times on a seeded BASELINE-shaped array -- an ncu target.
 
     python tools/route_once.py --config c4 --route box-complement [--box 16,16,16] [--reps 3]
+    python tools/route_once.py --config c1 --shape 4096,4096 --dtype int64 --op max --route bdbs --box 4,4
 """
 
 import argparse
@@ -18,6 +19,8 @@ def main():
     ap.add_argument("--box", default="")
     ap.add_argument("--shape", default="")
     ap.add_argument("--reps", type=int, default=3)
+    ap.add_argument("--dtype", default="", help="override the config's dtype (float32/float64/int64)")
+    ap.add_argument("--op", default="", help="add / max (int64 only)")
     args = ap.parse_args()
     import torch
 
@@ -29,7 +32,13 @@ def main():
         box = tuple(int(v) for v in args.box.split(","))
     shape = tuple(int(v) for v in args.shape.split(",")) if args.shape else None
     x = bench.make_input(args.config, "cuda", shape=shape)
+    if args.dtype:
+        dtype = args.dtype
+        x = x.to(getattr(torch, dtype)) if dtype != "int64" else (x * 2**20).to(torch.int64)
     ops = bench.ops_for(ex, dtype, args.route)
+    if args.op:
+        ops = {("int64", "max"): ex.IntMaxOps(), ("int64", "add"): ex.IntAddOps(),
+               ("float32", "add"): ex.Float32AddOps(), ("float64", "add"): ex.FloatAddOps()}[(dtype, args.op)]
     fn = {"bdbs": ex.bdbs_included, "bdbsc": ex.bdbs_excluded,
           "box-complement": ex.box_complement_excluded}[args.route]
     t = ex.Tensor(ops, x)
