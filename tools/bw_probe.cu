@@ -42,13 +42,18 @@ __global__ void k_copy(const int4* __restrict__ a, int4* __restrict__ b, size_t 
   for (; i < n16; i += stride) __stcs(b + i, __ldcs(a + i));
 }
 
-int main() {
+// argv[1] = "clean": after the memset flush, read a second 512 MB buffer so the lines the
+// timed kernel evicts are clean (no write-back of the flush's dirty lines inside the events)
+int main(int argc, char** argv) {
+  const bool clean = argc > 1 && argv[1][0] == 'c';
   const size_t sizes_mb[] = {64, 134, 268, 1074, 4295};
   int sms = 0; CK(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, 0));
   size_t maxb = 4295ull << 20;
   char *a, *b, *flush; unsigned long long* sink;
   CK(cudaMalloc(&a, maxb)); CK(cudaMalloc(&b, maxb)); CK(cudaMalloc(&flush, 512ull << 20));
   CK(cudaMalloc(&sink, 8));
+  char* flush2 = nullptr;
+  if (clean) { CK(cudaMalloc(&flush2, 512ull << 20)); CK(cudaMemset(flush2, 3, 512ull << 20)); }
   CK(cudaMemset(a, 1, maxb)); CK(cudaMemset(b, 0, maxb));
   cudaEvent_t e0, e1; CK(cudaEventCreate(&e0)); CK(cudaEventCreate(&e1));
   const int grids[] = {1, 2, 4, 8, 16};
@@ -60,6 +65,7 @@ int main() {
         float best = 1e30f, sum = 0.f; int reps = mb > 1000 ? 5 : 20;
         for (int r = 0; r < reps + 2; ++r) {
           CK(cudaMemsetAsync(flush, r, 512ull << 20));  // L2 flush outside the events
+          if (clean) k_read<<<sms * 8, 512>>>((const int4*)flush2, (512ull << 20) / 16, sink);
           CK(cudaEventRecord(e0));
           if (kind == 0) k_read<<<grid, 512>>>((const int4*)a, n16, sink);
           else if (kind == 1) k_write<<<grid, 512>>>((int4*)b, n16);
@@ -70,9 +76,9 @@ int main() {
         }
         // copy moves bytes/2 in + bytes/2 out: `bytes` of traffic like the others
         double gbs_best = bytes / (best * 1e-3) / 1e9, gbs_avg = bytes / (sum / reps * 1e-3) / 1e9;
-        printf("{\"kind\": \"%s\", \"traffic_MB\": %zu, \"grid\": %d, \"best_us\": %.2f, "
+        printf("{\"flush\": \"%s\", \"kind\": \"%s\", \"traffic_MB\": %zu, \"grid\": %d, \"best_us\": %.2f, "
                "\"avg_us\": %.2f, \"GBps_best\": %.0f, \"GBps_avg\": %.0f}\n",
-               kind == 0 ? "read" : kind == 1 ? "write" : "copy", mb, grid, best * 1e3,
+               clean ? "write+read" : "write", kind == 0 ? "read" : kind == 1 ? "write" : "copy", mb, grid, best * 1e3,
                sum / reps * 1e3, gbs_best, gbs_avg);
       }
     }

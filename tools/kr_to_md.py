@@ -16,7 +16,44 @@ except (OSError, KeyError, ValueError):
 NOMINAL = 8000.0
 
 
+def _ceilings():
+    """Same-size ceilings from tools/bw_probe.cu (profiles/r2_bw_probe.jsonl): the best grid's
+    average GB/s of a plain read / write / copy kernel per traffic size, L2 flushed the same
+    way as kernel_report does."""
+    best = {}
+    try:
+        for line in open(os.path.join(ROOT, "profiles", "r2_bw_probe.jsonl")):
+            r = json.loads(line)
+            key = (r["kind"], r["traffic_MB"])
+            best[key] = max(best.get(key, 0.0), float(r["GBps_avg"]))
+    except OSError:
+        pass
+    return best
+
+
+def _ceiling_gbs(best, name):
+    """Plain-kernel GB/s at this launch's traffic size (log-interpolated between probe sizes)."""
+    import math
+    if not best or "MB]" not in name:
+        return None
+    mb = float(name.split("[")[1].rstrip("MB]"))
+    base = name.split("[")[0]
+    kind = "read" if base in ("idem_scan", "total", "row_reduce") else \
+        "write" if base == "idem_bcast" else "copy"
+    pts = sorted((m, g) for (k, m), g in best.items() if k == kind)
+    if not pts or mb < pts[0][0] * 0.5:
+        return None
+    if mb <= pts[0][0]:
+        return pts[0][1]
+    for (m0, g0), (m1, g1) in zip(pts, pts[1:]):
+        if mb <= m1:
+            t = (math.log(mb) - math.log(m0)) / (math.log(m1) - math.log(m0))
+            return g0 + t * (g1 - g0)
+    return pts[-1][1]
+
+
 def main(path):
+    ceil = _ceilings()
     rows = []
     seen = set()
     for line in open(path):
@@ -29,8 +66,8 @@ def main(path):
             continue
         seen.add(key)
         rows.append(d)
-    print(f"| config | route | operator | box | step ms | G elem/s | pass (algorithmic MB) | pass ms | TB/s | of measured {PEAK / 1000:.2f} | of nominal 8 | dimension passes in the launch | >= 70% of measured (per dimension pass) |")
-    print("|---|---|---|---|---|---|---|---|---|---|---|---|---|")
+    print(f"| config | route | operator | box | step ms | G elem/s | pass (algorithmic MB) | pass ms | TB/s | of measured {PEAK / 1000:.2f} | of nominal 8 | of a plain kernel with the same traffic | dimension passes in the launch | >= 70% of measured (per dimension pass) |")
+    print("|---|---|---|---|---|---|---|---|---|---|---|---|---|---|")
     for d in rows:
         ks = d["kernels"] or {"(launch-bound, no per-launch records)": {"ms": 0, "GBps": 0}}
         nper = _passes_per_kernel(d)
@@ -45,8 +82,9 @@ def main(path):
                 mark += f" ({eq / PEAK:.2f} per pass)"
             lead = (f"| {d['config']} | {d['route']} | {d['op']} | {'x'.join(map(str, d['box']))} | "
                     f"{d['step_ms']:.3f} | {d['Gelem_s']:.1f} |") if first else "| | | | | | |"
+            cg = _ceiling_gbs(ceil, name)
             print(f"{lead} {name} | {k.get('ms', 0):.3f} | {gbs / 1000:.2f} | {gbs / PEAK:.2f} | "
-                  f"{gbs / NOMINAL:.2f} | {m if m else '--'} | {mark} |")
+                  f"{gbs / NOMINAL:.2f} | {f'{gbs / cg:.2f}' if cg else '--'} | {m if m else '--'} | {mark} |")
             first = False
 
 
