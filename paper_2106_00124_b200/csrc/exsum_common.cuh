@@ -79,9 +79,16 @@ __device__ __forceinline__ Vec<T, V> ld_stream(const T* p) {
   return r;
 }
 
+// EXSUM_ST_KEEP (measurement build): plain stores, so a small array's
+// intermediate stays in L2 for the next launch of the route
+#ifndef EXSUM_ST_KEEP
+#define EXSUM_ST_KEEP 0
+#endif
 template <class T, int V>
 __device__ __forceinline__ void st_stream(T* p, const Vec<T, V>& v) {
-  if constexpr (sizeof(T) * V == 16) {
+  if constexpr (EXSUM_ST_KEEP) {
+    *reinterpret_cast<Vec<T, V>*>(p) = v;
+  } else if constexpr (sizeof(T) * V == 16) {
     __stcs(reinterpret_cast<int4*>(p), *reinterpret_cast<const int4*>(&v));
   } else if constexpr (sizeof(T) * V == 8) {
     __stcs(reinterpret_cast<int2*>(p), *reinterpret_cast<const int2*>(&v));
@@ -98,7 +105,10 @@ __device__ __forceinline__ i64 ld1<i64>(const i64* p) {
   return (i64)__ldcs(reinterpret_cast<const long long*>(p));
 }
 template <class T>
-__device__ __forceinline__ void st1(T* p, T v) { __stcs(p, v); }
+__device__ __forceinline__ void st1(T* p, T v) {
+  if constexpr (EXSUM_ST_KEEP) *p = v;
+  else __stcs(p, v);
+}
 
 // 64-bit-safe warp shuffles.
 template <class T>
