@@ -5,7 +5,10 @@ values uniform [0,1), box (16,16,16), strong excluded sum via
 box-complement (the route the config names first; BDBSC is reported beside
 it under "routes").  A step is one box_complement_excluded call over the whole
 array with the input already resident in HBM.  The input (4 GiB) is 32x the
-126 MB L2, so no L2 flush is needed between steps.
+126 MB L2, so no L2 flush is needed between steps.  (The smaller configs,
+--config c1 / c2: a 512 MB buffer is written before every timed step, outside
+the step's events, and `value` comes from K steps with the per-launch profiler
+off; a second profiled set of K steps gives the per-kernel figures.)
 
 e2e: the same workload through the host-buffer C ABI from pinned memory, every
 step copying its 4 GiB input in and its 4 GiB result out: over the K steps
@@ -174,9 +177,15 @@ def bench_config(cfg, route, world, sharded_path):
     return {"workload": cfg, "description": desc, "extents": list(ext), "box": list(box),
             "route": route, "operator": _monoid_name(dtype, route),
             "parallelism": f"axis0-shards{world}" if sharded_path else "single-gpu",
-            "l2": "input 4 GiB >> 126 MB L2; no flush needed" if N * es > 2**30
-            else "input smaller than 4x L2",
+            "l2": "input 4 GiB >> 126 MB L2; no flush needed" if not _needs_flush(N * es)
+            else "input under 4x the 126 MB L2: a 512 MB buffer is written between timed steps "
+                 "(L2 flush), outside each step's events",
             "seed": 0}
+
+
+def _needs_flush(nbytes):
+    """Arrays under 4x the 126 MB L2 get an L2 flush between timed steps."""
+    return nbytes < 4 * 126e6
 
 
 def _monoid_name(dtype, route):
@@ -379,33 +388,49 @@ def main():
     del out
 
     # -- timed region: K steps, device events on the launching stream --------
-    _native.profile_enable(True)
+    flush = (torch.empty(512 * 2**20, dtype=torch.uint8, device=dev)
+             if _needs_flush(N * es // (world if sharded_path else 1)) else None)
     starts = [torch.cuda.Event(enable_timing=True) for _ in range(args.steps)]
     ends = [torch.cuda.Event(enable_timing=True) for _ in range(args.steps)]
-    launches = 0
-    if dist is not None:
-        dist.barrier()
-    torch.cuda.synchronize(dev)
-    # keep the GPU busy while the host enqueues the K steps (~0.2 ms of spin per
-    # step, before the first start event): the events then time the device's
-    # back-to-back execution of the steps, not the host's enqueue rate -- which
-    # bounds a small config (C1: ~16 us of Python per call), and which e2e keeps
-    torch.cuda._sleep(int(args.steps * 2e-4 * 1.965e9))
+
+    def timed_steps():
+        if dist is not None:
+            dist.barrier()
+        torch.cuda.synchronize(dev)
+        # keep the GPU busy while the host enqueues the K steps (~0.2 ms of spin per
+        # step, before the first start event): the events then time the device's
+        # back-to-back execution of the steps, not the host's enqueue rate -- which
+        # bounds a small config (C1: ~16 us of Python per call), and which e2e keeps
+        torch.cuda._sleep(int(args.steps * 2e-4 * 1.965e9))
+        for i in range(args.steps):
+            if flush is not None:
+                flush.fill_(i & 0xFF)  # before the start event: not in the step's time
+            starts[i].record(stream)
+            out = step()
+            ends[i].record(stream)
+            del out
+        torch.cuda.synchronize(dev)
+        return [a.elapsed_time(b) for a, b in zip(starts, ends)]
+
+    unprofiled_ms = None
+    if flush is not None:
+        # small configs (20-100 us per step): the per-launch events of the
+        # profiler cost several us per launch and switch graph replay off, so
+        # `value` comes from a first set of K steps with the profiler off and
+        # the per-kernel figures from a second, profiled set
+        timed_steps()  # captures the graph
+        unprofiled_ms = timed_steps()
+    _native.profile_enable(True)
     t_begin = time.time()
     launches0 = _native.total_launch_count()
-    for i in range(args.steps):
-        starts[i].record(stream)
-        out = step()
-        ends[i].record(stream)
-        del out
+    profiled_ms = timed_steps()
     launches = _native.total_launch_count() - launches0
-    torch.cuda.synchronize(dev)
     clocks.mark(t_begin, time.time())
     time.sleep(0.1)
     clocks.__exit__(None, None, None)
     if dist is not None:
         dist.barrier()
-    step_ms = [s.elapsed_time(e) for s, e in zip(starts, ends)]
+    step_ms = unprofiled_ms if unprofiled_ms is not None else profiled_ms
     prof = _native.profile_records()
     _native.profile_enable(False)
     total_ms = sum(step_ms)
@@ -431,7 +456,7 @@ def main():
         gbs = d["bytes"] / (d["ms"] / 1e3) / 1e9 if d["ms"] > 0 else 0.0
         kernels[name] = {"launches": d["launches"], "avg_ms": d["ms"] / d["launches"],
                          "bytes_per_launch": d["bytes"] / d["launches"], "GBps": gbs,
-                         "share_of_step": d["ms"] / total_ms if total_ms else None}
+                         "share_of_step": d["ms"] / sum(profiled_ms) if sum(profiled_ms) else None}
     roofline = None
     if dom is not None:
         d = per[dom]
@@ -603,6 +628,7 @@ def main():
             "kernels": kernels,
             "routes": routes,
             "gpu_launches": launches,
+            "profiled_ms_per_step": sum(profiled_ms) / args.steps,
             "clocks": clocks.summary(),
             "e2e": e2e,
             "cpu_baseline": cpu,
