@@ -66,6 +66,25 @@ namespace exsum {
 #ifndef FP_DEFER_STORE
 #define FP_DEFER_STORE 1  // 1: every mode but WIN_SLOW below; 2: every mode
 #endif
+// balanced unit ranges instead of uniform segments (go_pair): threshold in
+// percent over the even split, ranges per SM; EXSUM_FP_BALANCED=0 turns it off
+#ifndef FP_BALANCED_PCT
+#define FP_BALANCED_PCT 2
+#endif
+// windows along axis d-2 below this keep uniform segments under ROW_WIN
+// (measured: C5 f64 box 4^3 0.355 -> 0.364 ms, 2^3 0.353 -> 0.374 ms in balanced
+// mode; box 8^3 0.361 -> 0.340, 16^3 0.381 -> 0.363; the row rounds of
+// box-complement gain at every window: C5 box 2^3 0.384 -> 0.365)
+#ifndef FP_BALANCED_MIN_K_WIN
+#define FP_BALANCED_MIN_K_WIN 8
+#endif
+#ifndef FP_BALANCED_MULT
+#define FP_BALANCED_MULT 1
+#endif
+inline bool fp_balanced_on() {
+  const char* e = getenv("EXSUM_FP_BALANCED");
+  return !(e && e[0] == '0');
+}
 // Rows per streaming unit: 16 (a multiple of K1) for wide rows; narrow rows
 // (C <= 8: 64-thread CTAs whose shared ring and stage bound the CTAs per SM)
 // take 8-row units where K1 allows, doubling the resident CTAs.
@@ -161,16 +180,36 @@ k_fused_pair(const T* __restrict__ in, T* __restrict__ out, int64_t outer, int64
   const int64_t items = outer * nseg * nst;
   const bool kvec = (kx % VE) == 0;
 
-  for (int64_t item = blockIdx.x; item < items; item += gridDim.x) {
-    // strips fastest: the CTAs in flight cover whole rows
-    const int64_t strip = STRIP ? item % nst : 0;
-    const int64_t os = STRIP ? item / nst : item;
-    const int64_t o = os / nseg;
-    const int64_t seg = os % nseg;
+  // Balanced mode (seg_len < 0; nseg then holds the units per line): the
+  // outer * nseg units of the whole array are cut into gridDim.x equal
+  // contiguous ranges, one per CTA, each walked as one piece per line it
+  // touches -- few lines on one resident CTA per SM (a shard's 128 planes, C5's
+  // 512) otherwise lose a fraction of a wave or pay a halo per short segment.
+  const bool balanced = !STRIP && seg_len < 0;
+  int64_t item = balanced ? outer * nseg * (int64_t)blockIdx.x / gridDim.x : (int64_t)blockIdx.x;
+  const int64_t item_end = balanced ? outer * nseg * ((int64_t)blockIdx.x + 1) / gridDim.x : items;
+  while (item < item_end) {
+    int64_t strip, o, xs, xe;
+    if (balanced) {
+      o = item / nseg;
+      const int64_t us = item - o * nseg;
+      const int64_t cnt = nseg - us < item_end - item ? nseg - us : item_end - item;
+      strip = 0;
+      xs = us * U;
+      xe = (us + cnt) * U < n1 ? (us + cnt) * U : n1;
+      item += cnt;
+    } else {
+      // strips fastest: the CTAs in flight cover whole rows
+      strip = STRIP ? item % nst : 0;
+      const int64_t os = STRIP ? item / nst : item;
+      o = os / nseg;
+      const int64_t seg = os % nseg;
+      xs = seg * seg_len;  // multiple of U
+      xe = xs + seg_len < n1 ? xs + seg_len : n1;
+      item += gridDim.x;
+    }
     const bool last_strip = strip + 1 == nst;
     const bool loads = colthr && !(halo_thr && last_strip);  // no halo past the row end
-    const int64_t xs = seg * seg_len;  // multiple of U
-    const int64_t xe = xs + seg_len < n1 ? xs + seg_len : n1;
     const int64_t u0 = xs / U;
     const int64_t u_end = (xe + U - 1) / U;
     const T* src = in + o * n1 * rs + strip * N2 + col;
@@ -650,12 +689,27 @@ int go_pair(const T* in, T* out, int64_t outer, int64_t n1, int64_t kx,
   const int64_t nunits = (n1 + U - 1) / U;
   // segments per outer index (exsum_launch.h: wave rounding vs halo + fill)
   int64_t nseg = pick_segments(outer * nstrips, nunits, per_sm);
-  const int64_t seg_len = U * ((nunits + nseg - 1) / nseg);
+  int64_t seg_len = U * ((nunits + nseg - 1) / nseg);
   nseg = (n1 + seg_len - 1) / seg_len;
   const int64_t items = outer * nseg * nstrips;
   int64_t grid = items;
   const int64_t cap = (int64_t)num_sms() * per_sm * 4;
   if (grid > cap) grid = cap;
+  // one resident CTA per SM and few lines: when the best uniform segmentation
+  // still costs FP_BALANCED_PCT % more than an even split of the units (a
+  // partial last wave, or a halo block per short segment), cut the units
+  // into one contiguous range per SM instead (balanced mode of the kernel)
+  if (!STRIP && per_sm == 1 && (MODE != ROW_WIN || K1 >= FP_BALANCED_MIN_K_WIN) && fp_balanced_on()) {
+    const int64_t slots = num_sms();
+    const int64_t per = seg_len / U;
+    const double uniform = (double)((items + slots - 1) / slots) * ((double)per + 1.0);
+    const double even = (double)(outer * nunits) / (double)slots + 2.0;
+    if (outer * nunits >= 4 * slots && uniform * 100.0 > even * (100.0 + FP_BALANCED_PCT)) {
+      seg_len = -1;
+      nseg = nunits;
+      grid = slots * FP_BALANCED_MULT;
+    }
+  }
   ensure_smem((const void*)k_fused_pair<T, Op, C, K1, MODE, TV, STRIP>, smem);
   k_fused_pair<T, Op, C, K1, MODE, TV, STRIP><<<(unsigned)grid, NTA, smem, s>>>(
       in, out, outer, n1, kx, seg_len, nseg, total, Tail, STRIP ? n2full : (int64_t)N2, nstrips);

@@ -167,8 +167,10 @@ class CudaEngine:
         return out
 
     def bc_tail_ok(self, ext, k):
-        """Whether the per-shard tail applies (3-D: R is n0 x n1)."""
-        if len(ext) != 3:
+        """Whether the per-shard tail applies: `ext` / `k` are R's extents and
+        box, i.e. the array's without the last axis, and R must be 2-D (a 3-D
+        array: R is n0 x n1)."""
+        if len(ext) != 2:
             return False
         rc = self.L.exsum_shard_bc_tail(-1, None, None, None, _native.DTYPE[self.dtype_name],
                                          _native.OP[self.op], int(ext[0]), int(ext[1]), int(k[0]),
@@ -534,11 +536,13 @@ class _Done:
         return None
 
 
-def run_loopback(route, ops, a, box, world, engine, split=True):
+def run_loopback(route, ops, a, box, world, engine, split=True, concat=True):
     """Run the sharded route with `world` virtual ranks in this process (one
     GPU): halos are sliced from the global array, the combine step sees every
     rank's stage-1 output.  Returns the concatenated output.  This exercises
-    the same stage entry points and slab arithmetic as the multi-process path."""
+    the same stage entry points and slab arithmetic as the multi-process path.
+    concat=False returns the per-rank outputs as a list (no 2 N s concatenation:
+    tools/sharded_rank_time.py times the ranks' stages alone)."""
     import torch
 
     ext = tuple(int(v) for v in a.shape)
@@ -550,7 +554,7 @@ def run_loopback(route, ops, a, box, world, engine, split=True):
                        for r in runners]
         marg = comm.all_reduce_max(None)
         outs = [engine.idem_write(marg, ext, r.k, r.start, r.n_own) for r in runners if r.n_own > 0]
-        return torch.cat(outs, dim=0)
+        return torch.cat(outs, dim=0) if concat else outs
     ys, extras = [], []
     for r in runners:
         x_ext = a[r.start:r.end + r.halo]
@@ -569,13 +573,13 @@ def run_loopback(route, ops, a, box, world, engine, split=True):
             o = r.stage2(y, T)
             if o is not None:
                 outs.append(o)
-        return torch.cat(outs, dim=0)
+        return torch.cat(outs, dim=0) if concat else outs
     combined = runners[0].combine(extras[0], a.device) if world > 0 else None
     for r, y in zip(runners, ys):
         o = r.stage2(y, combined)
         if o is not None:
             outs.append(o)
-    return torch.cat(outs, dim=0)
+    return torch.cat(outs, dim=0) if concat else outs
 
 
 def make_local_slab(gen_planes, ext, rank, world, box=None):

@@ -24,6 +24,14 @@ CASES = [
     ((5, 8, 8), (8, 2, 2), "add-i64", 2),        # one empty rank
     ((5, 8, 8), (8, 2, 2), "max-i64", 2),        # marginal form with an empty rank
     ((33, 17, 66), (4, 5, 8), "max-i64", 4),     # marginal form, uneven slabs, odd rows
+    # the own-rows tail (exsum_shard_bc_tail) on uneven slabs, k1 = n1, k1 = 1, one
+    # block along axis 0 (a single non-empty rank), more ranks than blocks
+    ((33, 17, 66), (4, 5, 8), "add-i64", 4),
+    ((40, 7, 19), (3, 7, 2), "add-f64", 5),
+    ((16, 16, 16), (16, 1, 4), "add-i64", 2),
+    ((130, 33, 40), (8, 33, 5), "add-i64", 8),
+    ((12, 260, 24), (5, 9, 3), "add-f32", 6),
+    ((1024, 64, 32), (16, 16, 16), "add-f32", 8),
 ]
 
 
@@ -44,6 +52,28 @@ def test_sharded_max_takes_the_marginal_form():
     a = np.random.default_rng(1).integers(-2**40, 2**40, size=ext, dtype=np.int64)
     got = run_loopback("box-complement", ops, torch.from_numpy(a).cuda(), box, 3, engine)
     assert np.array_equal(got.cpu().numpy(), orc.box_complement_excluded(a, box, "max"))
+
+
+def test_sharded_3d_box_complement_takes_the_own_rows_tail():
+    """A 3-D box-complement over + computes only its own rows of the tail on
+    every rank (exsum_shard_bc_tail: R2 all-gathered, R's halo rows exchanged)
+    -- the route the loopback cases below must be exercising."""
+    import torch
+
+    import paper_2106_00124_b200 as ex
+    from paper_2106_00124_b200.sharded import CudaEngine, ShardedRunner
+
+    dev = torch.device("cuda")
+    for mono, ext, box in (("add-i64", (37, 20, 28), (4, 3, 5)), ("add-f32", (64, 96, 256), (8, 8, 8)),
+                           ("add-f32", (1024, 1024, 1024), (16, 16, 16)), ("add-f64", (45, 12, 32), (20, 4, 4))):
+        ops = ex.resolve_monoid(mono)
+        r = ShardedRunner("box-complement", ops, ext, box, 1, 3, dev, comm=object(),
+                          engine=CudaEngine(ops, dev))
+        assert r.own_tail and not r.idem, (mono, ext)
+    ops = ex.resolve_monoid("add-f64")  # d = 2: R is 1-D, the tail is all-gathered
+    r = ShardedRunner("box-complement", ops, (50, 40), (16, 7), 1, 3, dev, comm=object(),
+                      engine=CudaEngine(ops, dev))
+    assert not r.own_tail
 
 
 @pytest.mark.parametrize("ext,box,mono,world", CASES, ids=lambda v: str(v))
