@@ -23,6 +23,8 @@
 //   EX == 2: the BDBSC total, folded per thread from registers.
 #pragma once
 
+#include <stdlib.h>
+
 #include <type_traits>
 
 #include "exsum_common.cuh"
@@ -55,12 +57,27 @@ namespace exsum {
 #define AS_NO_C32 0  // measurement only: 1 keeps 4-byte types on the 512-column strip
 #endif
 
+// the last partial wave of whole-line items as balanced unit ranges (see the
+// kernel); AS_BAL_GU_MULT > 0 caps the CTAs of the uniform part at that many
+// per SM (grid-strided) instead of one CTA per line; EXSUM_AS_BAL_TAIL=0: off
+#ifndef AS_BAL_TAIL
+#define AS_BAL_TAIL 1
+#endif
+#ifndef AS_BAL_GU_MULT
+#define AS_BAL_GU_MULT 0
+#endif
+inline bool as_bal_tail_on() {
+  const char* e = getenv("EXSUM_AS_BAL_TAIL");
+  return !(e && e[0] == '0');
+}
+
 template <class T, class Op, int C, int K1, int EX>
 __global__ void __launch_bounds__(32 * C / (16 / sizeof(T)), 1)
 k_axis_stream(const T* __restrict__ in, T* __restrict__ out, int64_t outer, int64_t n1,
               int64_t inner, int64_t nout, int64_t seg_len, int64_t nseg,
               const typename AccOf<T>::type* __restrict__ total, T* __restrict__ rowpart,
-              int64_t row_len, typename AccOf<T>::type* __restrict__ tpart) {
+              int64_t row_len, typename AccOf<T>::type* __restrict__ tpart, int64_t bal_line0,
+              int bal_ctas) {
   typedef typename AccOf<T>::type Acc;
   constexpr int VE = 16 / sizeof(T);
   constexpr int N2 = 32 * C;                     // strip width (columns)
@@ -87,14 +104,39 @@ k_axis_stream(const T* __restrict__ in, T* __restrict__ out, int64_t outer, int6
 #pragma unroll
   for (int j = 0; j < VE; ++j) tacc[j] = Op::template identity<Acc>();
 
-  for (int64_t item = blockIdx.x; item < items; item += gridDim.x) {
-    const int64_t it2 = AS_SEG_FAST ? (item % nseg) * (outer * strips) + item / nseg : item;
-    const int64_t strip = AS_PSTRIDE == 1 ? it2 % strips : (it2 % strips) * AS_PSTRIDE % strips;
-    const int64_t rest = it2 / strips;
-    const int64_t o = rest % outer;
-    const int64_t seg = rest / outer;
-    const int64_t xs = seg * seg_len;  // multiple of U
-    const int64_t xe = xs + seg_len < nout ? xs + seg_len : nout;
+  // Balanced tail (bal_ctas > 0; whole-line items, nseg == 1): the lines
+  // [0, bal_line0) -- whole waves of one line per SM -- run as uniform items
+  // on the first gridDim.x - bal_ctas CTAs; the units of the remaining lines
+  // (less than one wave of lines) are cut into bal_ctas equal contiguous
+  // ranges, one per CTA, so the last wave ends together instead of leaving
+  // the SMs without a line idle for a whole item.
+  const int64_t gu = (int64_t)gridDim.x - bal_ctas;
+  const bool bal = bal_ctas > 0 && (int64_t)blockIdx.x >= gu;
+  const int64_t nun = (nout + U - 1) / U;  // units per line
+  const int64_t tail_units = (outer * strips - bal_line0) * nun;
+  int64_t item = bal ? tail_units * ((int64_t)blockIdx.x - gu) / bal_ctas : (int64_t)blockIdx.x;
+  const int64_t item_end = bal ? tail_units * ((int64_t)blockIdx.x - gu + 1) / bal_ctas
+                               : (bal_ctas > 0 ? bal_line0 : items);
+  while (item < item_end) {
+    int64_t strip, o, xs, xe;
+    if (bal) {
+      const int64_t l = item / nun, us = item - l * nun;
+      const int64_t cnt = nun - us < item_end - item ? nun - us : item_end - item;
+      strip = (bal_line0 + l) % strips;
+      o = (bal_line0 + l) / strips;
+      xs = us * U;
+      xe = (us + cnt) * U < nout ? (us + cnt) * U : nout;
+      item += cnt;
+    } else {
+      const int64_t it2 = AS_SEG_FAST ? (item % nseg) * (outer * strips) + item / nseg : item;
+      strip = AS_PSTRIDE == 1 ? it2 % strips : (it2 % strips) * AS_PSTRIDE % strips;
+      const int64_t rest = it2 / strips;
+      o = rest % outer;
+      const int64_t seg = rest / outer;
+      xs = seg * seg_len;  // multiple of U
+      xe = xs + seg_len < nout ? xs + seg_len : nout;
+      item += gu;
+    }
     const int64_t u0 = xs / U;
     const int64_t u_end = (xe + U - 1) / U;
     const T* src = in + o * n1 * inner + strip * N2 + col;
@@ -328,11 +370,23 @@ int go_axis_stream_c(const T* in, T* out, int64_t outer, int64_t n, int64_t inne
   const int64_t cap = (int64_t)num_sms() * per_sm * AS_GRID_MULT;
   if (EX == 2 && cap > ex->cap) return -1;
   if (grid > cap) grid = cap;
+  // whole-line items on one resident CTA per SM whose count is not a multiple
+  // of the SM count: the last partial wave of lines as balanced unit ranges
+  int64_t bal_line0 = 0;
+  int bal_ctas = 0;
+  const int64_t slots = (int64_t)num_sms() * per_sm;
+  if (AS_BAL_TAIL && per_sm == 1 && nseg == 1 && EX != 2 && AS_SEG_FAST == 0 && AS_PSTRIDE == 1 &&
+      lines > slots && lines % slots != 0 && nunits >= 8 && as_bal_tail_on()) {
+    bal_line0 = (lines / slots) * slots;
+    bal_ctas = (int)slots;
+    grid = (AS_BAL_GU_MULT > 0 && bal_line0 > slots * AS_BAL_GU_MULT ? slots * AS_BAL_GU_MULT
+                                                                       : bal_line0) + bal_ctas;
+  }
   ensure_smem((const void*)k_axis_stream<T, Op, C, K1, EX>, smem);
   k_axis_stream<T, Op, C, K1, EX><<<(unsigned)grid, NT, smem, s>>>(
       in, out, outer, n, inner, nout, seg_len, nseg, total,
       EX == 1 ? (T*)ex->buf : nullptr, EX == 1 ? ex->row_len : N2,
-      EX == 2 ? (Acc*)ex->buf : nullptr);
+      EX == 2 ? (Acc*)ex->buf : nullptr, bal_line0, bal_ctas);
   if (ex) {
     ex->n_out_done = 1;
     if (EX == 1) {
