@@ -66,9 +66,11 @@ namespace exsum {
 #ifndef AS_BAL_GU_MULT
 #define AS_BAL_GU_MULT 0
 #endif
-inline bool as_bal_tail_on() {
+// EXSUM_AS_BAL_TAIL: 0 off, 1 (default) where whole-line items were chosen,
+// 2 whole-line items and a balanced last wave whenever the lines allow it (tests)
+inline int as_bal_tail_mode() {
   const char* e = getenv("EXSUM_AS_BAL_TAIL");
-  return !(e && e[0] == '0');
+  return e && e[0] >= '0' && e[0] <= '2' ? e[0] - '0' : 1;
 }
 
 template <class T, class Op, int C, int K1, int EX>
@@ -363,6 +365,11 @@ int go_axis_stream_c(const T* in, T* out, int64_t outer, int64_t n, int64_t inne
   const int64_t nunits = (nout + U - 1) / U;
   int64_t nseg = pick_segments(lines, nunits, per_sm);
   if (nseg < AS_NSEG_MIN && nunits >= AS_NSEG_MIN) nseg = AS_NSEG_MIN;
+  const int bal_mode = AS_BAL_TAIL ? as_bal_tail_mode() : 0;
+  const int64_t slots = (int64_t)num_sms() * per_sm;
+  const bool bal_shape = per_sm == 1 && EX != 2 && AS_SEG_FAST == 0 && AS_PSTRIDE == 1 &&
+                         lines > slots && lines % slots != 0;
+  if (bal_mode == 2 && bal_shape) nseg = 1;
   const int64_t seg_len = U * ((nunits + nseg - 1) / nseg);
   nseg = (nout + seg_len - 1) / seg_len;
   const int64_t items = lines * nseg;
@@ -374,9 +381,7 @@ int go_axis_stream_c(const T* in, T* out, int64_t outer, int64_t n, int64_t inne
   // of the SM count: the last partial wave of lines as balanced unit ranges
   int64_t bal_line0 = 0;
   int bal_ctas = 0;
-  const int64_t slots = (int64_t)num_sms() * per_sm;
-  if (AS_BAL_TAIL && per_sm == 1 && nseg == 1 && EX != 2 && AS_SEG_FAST == 0 && AS_PSTRIDE == 1 &&
-      lines > slots && lines % slots != 0 && nunits >= 8 && as_bal_tail_on()) {
+  if (bal_mode && bal_shape && nseg == 1 && (nunits >= 8 || bal_mode == 2)) {
     bal_line0 = (lines / slots) * slots;
     bal_ctas = (int)slots;
     grid = (AS_BAL_GU_MULT > 0 && bal_line0 > slots * AS_BAL_GU_MULT ? slots * AS_BAL_GU_MULT

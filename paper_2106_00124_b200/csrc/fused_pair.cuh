@@ -81,9 +81,11 @@ namespace exsum {
 #ifndef FP_BALANCED_MULT
 #define FP_BALANCED_MULT 1
 #endif
-inline bool fp_balanced_on() {
+// EXSUM_FP_BALANCED: 0 off, 1 (default) by the cost model, 2 whenever the
+// kernel allows it (tests: balanced ranges on small arrays, every window)
+inline int fp_balanced_mode() {
   const char* e = getenv("EXSUM_FP_BALANCED");
-  return !(e && e[0] == '0');
+  return e && e[0] >= '0' && e[0] <= '2' ? e[0] - '0' : 1;
 }
 // Rows per streaming unit: 16 (a multiple of K1) for wide rows; narrow rows
 // (C <= 8: 64-thread CTAs whose shared ring and stage bound the CTAs per SM)
@@ -699,12 +701,15 @@ int go_pair(const T* in, T* out, int64_t outer, int64_t n1, int64_t kx,
   // still costs FP_BALANCED_PCT % more than an even split of the units (a
   // partial last wave, or a halo block per short segment), cut the units
   // into one contiguous range per SM instead (balanced mode of the kernel)
-  if (!STRIP && per_sm == 1 && (MODE != ROW_WIN || K1 >= FP_BALANCED_MIN_K_WIN) && fp_balanced_on()) {
+  const int bal_mode = fp_balanced_mode();
+  if (!STRIP && per_sm == 1 && bal_mode &&
+      (bal_mode == 2 || MODE != ROW_WIN || K1 >= FP_BALANCED_MIN_K_WIN)) {
     const int64_t slots = num_sms();
     const int64_t per = seg_len / U;
     const double uniform = (double)((items + slots - 1) / slots) * ((double)per + 1.0);
     const double even = (double)(outer * nunits) / (double)slots + 2.0;
-    if (outer * nunits >= 4 * slots && uniform * 100.0 > even * (100.0 + FP_BALANCED_PCT)) {
+    if (bal_mode == 2 ||
+        (outer * nunits >= 4 * slots && uniform * 100.0 > even * (100.0 + FP_BALANCED_PCT))) {
       seg_len = -1;
       nseg = nunits;
       grid = slots * FP_BALANCED_MULT;
