@@ -81,6 +81,9 @@ namespace exsum {
 #ifndef FP_BALANCED_MULT
 #define FP_BALANCED_MULT 1
 #endif
+#ifndef FP_BALANCED_TAIL
+#define FP_BALANCED_TAIL 1
+#endif
 // EXSUM_FP_BALANCED: 0 off, 1 (default) by the cost model, 2 whenever the
 // kernel allows it (tests: balanced ranges on small arrays, every window)
 inline int fp_balanced_mode() {
@@ -129,7 +132,7 @@ __global__ void __launch_bounds__(32 * C / TV + (STRIP ? 32 : 0),
 k_fused_pair(const T* __restrict__ in, T* __restrict__ out, int64_t outer, int64_t n1,
              int64_t kx, int64_t seg_len, int64_t nseg,
              const typename AccOf<T>::type* __restrict__ total, const T* __restrict__ Tail,
-             int64_t n2full, int64_t nstrips) {
+             int64_t n2full, int64_t nstrips, int64_t bal_line0, int bal_ctas) {
   constexpr int VE = 16 / sizeof(T);  // 16-byte vector (stage layout, row op)
   constexpr int N2 = 32 * C;           // row length
   constexpr int NT = N2 / TV;          // threads: one TV-element column vector each
@@ -182,20 +185,27 @@ k_fused_pair(const T* __restrict__ in, T* __restrict__ out, int64_t outer, int64
   const int64_t items = outer * nseg * nst;
   const bool kvec = (kx % VE) == 0;
 
-  // Balanced mode (seg_len < 0; nseg then holds the units per line): the
-  // outer * nseg units of the whole array are cut into gridDim.x equal
+  // Balanced ranges (bal_ctas > 0, no strips): the lines [0, bal_line0) run as
+  // uniform (line, segment) items on the first gridDim.x - bal_ctas CTAs; the
+  // units of the lines from bal_line0 on are cut into bal_ctas equal
   // contiguous ranges, one per CTA, each walked as one piece per line it
-  // touches -- few lines on one resident CTA per SM (a shard's 128 planes, C5's
-  // 512) otherwise lose a fraction of a wave or pay a halo per short segment.
-  const bool balanced = !STRIP && seg_len < 0;
-  int64_t item = balanced ? outer * nseg * (int64_t)blockIdx.x / gridDim.x : (int64_t)blockIdx.x;
-  const int64_t item_end = balanced ? outer * nseg * ((int64_t)blockIdx.x + 1) / gridDim.x : items;
+  // touches.  bal_line0 = 0: the whole array that way (few lines on one
+  // resident CTA per SM -- a shard's 128 planes, C5's 512 -- otherwise lose a
+  // fraction of a wave or pay a halo per short segment); bal_line0 = whole
+  // waves of lines: only the last partial wave is balanced.
+  const int64_t gu = (int64_t)gridDim.x - bal_ctas;
+  const bool bal = !STRIP && bal_ctas > 0 && (int64_t)blockIdx.x >= gu;
+  const int64_t nun = (n1 + U - 1) / U;  // units per line
+  const int64_t bal_units = (outer - bal_line0) * nun;
+  int64_t item = bal ? bal_units * ((int64_t)blockIdx.x - gu) / bal_ctas : (int64_t)blockIdx.x;
+  const int64_t item_end = bal ? bal_units * ((int64_t)blockIdx.x - gu + 1) / bal_ctas
+                               : (!STRIP && bal_ctas > 0 ? bal_line0 * nseg : items);
   while (item < item_end) {
     int64_t strip, o, xs, xe;
-    if (balanced) {
-      o = item / nseg;
-      const int64_t us = item - o * nseg;
-      const int64_t cnt = nseg - us < item_end - item ? nseg - us : item_end - item;
+    if (bal) {
+      const int64_t l = item / nun, us = item - l * nun;
+      const int64_t cnt = nun - us < item_end - item ? nun - us : item_end - item;
+      o = bal_line0 + l;
       strip = 0;
       xs = us * U;
       xe = (us + cnt) * U < n1 ? (us + cnt) * U : n1;
@@ -208,7 +218,7 @@ k_fused_pair(const T* __restrict__ in, T* __restrict__ out, int64_t outer, int64
       const int64_t seg = os % nseg;
       xs = seg * seg_len;  // multiple of U
       xe = xs + seg_len < n1 ? xs + seg_len : n1;
-      item += gridDim.x;
+      item += bal_ctas > 0 ? gu : (int64_t)gridDim.x;
     }
     const bool last_strip = strip + 1 == nst;
     const bool loads = colthr && !(halo_thr && last_strip);  // no halo past the row end
@@ -700,24 +710,36 @@ int go_pair(const T* in, T* out, int64_t outer, int64_t n1, int64_t kx,
   // one resident CTA per SM and few lines: when the best uniform segmentation
   // still costs FP_BALANCED_PCT % more than an even split of the units (a
   // partial last wave, or a halo block per short segment), cut the units
-  // into one contiguous range per SM instead (balanced mode of the kernel)
+  // into one contiguous range per SM instead (balanced ranges of the kernel).
+  // The windowed row op with a small window measured slower that way; with
+  // more lines than SMs it keeps whole-line items for the full waves of lines
+  // and balances only the last partial wave (FP_BALANCED_TAIL)
   const int bal_mode = fp_balanced_mode();
-  if (!STRIP && per_sm == 1 && bal_mode &&
-      (bal_mode == 2 || MODE != ROW_WIN || K1 >= FP_BALANCED_MIN_K_WIN)) {
+  int64_t bal_line0 = 0;
+  int bal_ctas = 0;
+  if (!STRIP && per_sm == 1 && bal_mode) {
     const int64_t slots = num_sms();
     const int64_t per = seg_len / U;
     const double uniform = (double)((items + slots - 1) / slots) * ((double)per + 1.0);
     const double even = (double)(outer * nunits) / (double)slots + 2.0;
-    if (bal_mode == 2 ||
-        (outer * nunits >= 4 * slots && uniform * 100.0 > even * (100.0 + FP_BALANCED_PCT))) {
-      seg_len = -1;
-      nseg = nunits;
-      grid = slots * FP_BALANCED_MULT;
+    const bool pays = bal_mode == 2 || (outer * nunits >= 4 * slots &&
+                                        uniform * 100.0 > even * (100.0 + FP_BALANCED_PCT));
+    const bool small_win = MODE == ROW_WIN && K1 < FP_BALANCED_MIN_K_WIN;
+    if (pays && (!small_win || bal_mode == 2)) {
+      bal_ctas = (int)(slots * FP_BALANCED_MULT);
+      grid = bal_ctas;
+    } else if (pays && FP_BALANCED_TAIL && outer > slots && outer % slots != 0) {
+      bal_line0 = (outer / slots) * slots;
+      bal_ctas = (int)slots;
+      nseg = 1;
+      seg_len = U * nunits;
+      grid = bal_line0 + bal_ctas;  // one whole line per CTA, then the ranges
     }
   }
   ensure_smem((const void*)k_fused_pair<T, Op, C, K1, MODE, TV, STRIP>, smem);
   k_fused_pair<T, Op, C, K1, MODE, TV, STRIP><<<(unsigned)grid, NTA, smem, s>>>(
-      in, out, outer, n1, kx, seg_len, nseg, total, Tail, STRIP ? n2full : (int64_t)N2, nstrips);
+      in, out, outer, n1, kx, seg_len, nseg, total, Tail, STRIP ? n2full : (int64_t)N2, nstrips,
+      bal_line0, bal_ctas);
   return 1;
 }
 
