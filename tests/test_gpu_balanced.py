@@ -81,3 +81,46 @@ def test_balanced_schedules_match_the_oracle(mono, ext, box, monkeypatch):
         monkeypatch.delenv("EXSUM_FP_BALANCED")
         monkeypatch.delenv("EXSUM_AS_BAL_TAIL")
         assert np.array_equal(got.view(np.uint8), plain.view(np.uint8)), route
+
+
+def test_balanced_schedules_random_shapes(monkeypatch):
+    """Random ragged shapes on the one-CTA-per-SM row widths with the balanced
+    schedules forced: every route against the schedules switched off, bit for
+    bit (the uniform schedules are pinned to the oracle by the other suites),
+    and BDBS against the oracle directly."""
+    import torch
+
+    import paper_2106_00124_b200 as ex
+
+    rng = np.random.default_rng(int(os.environ.get("EXSUM_FUZZ_SEED", "2106")) + 77)
+    n_cases = int(os.environ.get("EXSUM_BALANCED_CASES", "20"))
+    fns = {"bdbs": ex.bdbs_included, "bdbsc": ex.bdbs_excluded,
+           "box-complement": ex.box_complement_excluded}
+    for case in range(n_cases):
+        mono = str(rng.choice(["add-f32", "add-f64", "add-i64", "max-i64"]))
+        width = 1024 if mono == "add-f32" else 512
+        n1 = int(rng.integers(3, 400))
+        lead = tuple(int(v) for v in rng.integers(1, 40, size=int(rng.integers(1, 3))))
+        if rng.random() < 0.3:  # many strips for the axis pass: a long axis 0 over >= 149 strips
+            lead, n1 = (int(rng.integers(64, 200)),), int(rng.integers(149, 330))
+        ext = lead + (n1, width)
+        k = int(rng.choice([2, 4, 8, 16]))
+        box = tuple(int(rng.choice([1, k, 3, n])) if rng.random() < 0.25 else k for n in ext)
+        ops = ex.resolve_monoid(mono)
+        a = _data(mono, ext, seed=1000 + case)
+        x = torch.from_numpy(a).cuda()
+        op = "max" if mono == "max-i64" else "add"
+        routes = ["bdbs", "box-complement"] + (["bdbsc"] if ops.has_inverse else [])
+        for route in routes:
+            monkeypatch.setenv("EXSUM_FP_BALANCED", "2")
+            monkeypatch.setenv("EXSUM_AS_BAL_TAIL", "2")
+            forced = fns[route](ex.Tensor(ops, x), box).data.cpu().numpy()
+            monkeypatch.setenv("EXSUM_FP_BALANCED", "0")
+            monkeypatch.setenv("EXSUM_AS_BAL_TAIL", "0")
+            plain = fns[route](ex.Tensor(ops, x), box).data.cpu().numpy()
+            monkeypatch.delenv("EXSUM_FP_BALANCED")
+            monkeypatch.delenv("EXSUM_AS_BAL_TAIL")
+            assert np.array_equal(forced.view(np.uint8), plain.view(np.uint8)), (case, mono, ext, box, route)
+            if route == "bdbs":
+                want = orc.ROUTES[route](a, box, op)
+                assert np.array_equal(forced.view(np.uint8), want.view(np.uint8)), (case, mono, ext, box)
