@@ -84,6 +84,10 @@ namespace exsum {
 #ifndef FP_BALANCED_TAIL
 #define FP_BALANCED_TAIL 1
 #endif
+// strips (rows longer than the widest row template) take the balanced schedules too
+#ifndef FP_BALANCED_STRIPS
+#define FP_BALANCED_STRIPS 1
+#endif
 // EXSUM_FP_BALANCED: 0 off, 1 (default) by the cost model, 2 whenever the
 // kernel allows it (tests: balanced ranges on small arrays, every window)
 inline int fp_balanced_mode() {
@@ -194,19 +198,20 @@ k_fused_pair(const T* __restrict__ in, T* __restrict__ out, int64_t outer, int64
   // fraction of a wave or pay a halo per short segment); bal_line0 = whole
   // waves of lines: only the last partial wave is balanced.
   const int64_t gu = (int64_t)gridDim.x - bal_ctas;
-  const bool bal = !STRIP && bal_ctas > 0 && (int64_t)blockIdx.x >= gu;
+  // (with strips a line is one strip of one outer index, strips fastest)
+  const bool bal = bal_ctas > 0 && (int64_t)blockIdx.x >= gu;
   const int64_t nun = (n1 + U - 1) / U;  // units per line
-  const int64_t bal_units = (outer - bal_line0) * nun;
+  const int64_t bal_units = (outer * nst - bal_line0) * nun;
   int64_t item = bal ? bal_units * ((int64_t)blockIdx.x - gu) / bal_ctas : (int64_t)blockIdx.x;
   const int64_t item_end = bal ? bal_units * ((int64_t)blockIdx.x - gu + 1) / bal_ctas
-                               : (!STRIP && bal_ctas > 0 ? bal_line0 * nseg : items);
+                               : (bal_ctas > 0 ? bal_line0 * nseg : items);
   while (item < item_end) {
     int64_t strip, o, xs, xe;
     if (bal) {
       const int64_t l = item / nun, us = item - l * nun;
       const int64_t cnt = nun - us < item_end - item ? nun - us : item_end - item;
-      o = bal_line0 + l;
-      strip = 0;
+      strip = STRIP ? (bal_line0 + l) % nst : 0;
+      o = STRIP ? (bal_line0 + l) / nst : bal_line0 + l;
       xs = us * U;
       xe = (us + cnt) * U < n1 ? (us + cnt) * U : n1;
       item += cnt;
@@ -717,19 +722,20 @@ int go_pair(const T* in, T* out, int64_t outer, int64_t n1, int64_t kx,
   const int bal_mode = fp_balanced_mode();
   int64_t bal_line0 = 0;
   int bal_ctas = 0;
-  if (!STRIP && per_sm == 1 && bal_mode) {
+  if ((!STRIP || FP_BALANCED_STRIPS) && per_sm == 1 && bal_mode) {
     const int64_t slots = num_sms();
+    const int64_t lines = outer * nstrips;
     const int64_t per = seg_len / U;
     const double uniform = (double)((items + slots - 1) / slots) * ((double)per + 1.0);
-    const double even = (double)(outer * nunits) / (double)slots + 2.0;
-    const bool pays = bal_mode == 2 || (outer * nunits >= 4 * slots &&
+    const double even = (double)(lines * nunits) / (double)slots + 2.0;
+    const bool pays = bal_mode == 2 || (lines * nunits >= 4 * slots &&
                                         uniform * 100.0 > even * (100.0 + FP_BALANCED_PCT));
     const bool small_win = MODE == ROW_WIN && K1 < FP_BALANCED_MIN_K_WIN;
     if (pays && (!small_win || bal_mode == 2)) {
       bal_ctas = (int)(slots * FP_BALANCED_MULT);
       grid = bal_ctas;
-    } else if (pays && FP_BALANCED_TAIL && outer > slots && outer % slots != 0) {
-      bal_line0 = (outer / slots) * slots;
+    } else if (pays && FP_BALANCED_TAIL && lines > slots && lines % slots != 0) {
+      bal_line0 = (lines / slots) * slots;
       bal_ctas = (int)slots;
       nseg = 1;
       seg_len = U * nunits;

@@ -35,6 +35,11 @@ CASES = [
     ("add-f32", (130, 200, 1024), (16, 2, 4)),     # axis pass: 200 strips of 9 units, k < 8 pair
     ("add-f64", (70, 301, 512), (4, 4, 4)),        # axis pass: 301 strips of 5 units
     ("add-f32", (5, 40, 1024), (2, 8, 8)),         # fewer units than SMs: empty ranges
+    # strips (rows longer than the widest row template): a line is one strip of one outer index
+    ("add-f32", (3, 210, 3072), (2, 16, 16)),
+    ("add-f32", (170, 2048), (8, 8)),
+    ("add-f64", (2, 157, 1536), (2, 16, 16)),
+    ("max-i64", (7, 100, 1024), (1, 16, 16)),
 ]
 
 
